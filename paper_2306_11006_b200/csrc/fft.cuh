@@ -1,0 +1,187 @@
+// fft.cuh -- warp-level negacyclic FP64 FFT for the blind rotation.
+//
+// A real polynomial a(X) mod X^N + 1 is folded into M = N/2 complex points
+//   z[m] = (a[m] + i a[m+M]) * e^{i pi m / N}
+// whose length-M DFT (kernel e^{+2 pi i / M}) evaluates a at the N/2 roots
+// e^{i pi (4k+1)/N}; the other N/2 roots are their conjugates (SURVEY.md
+// Appendix B).  One warp owns one transform:
+//   M = P * L with L = 2P lanes, P complex values per lane,
+//   F1  in-register DIF DFT-P over m1 (input z[L*m1 + lane])
+//   tw  lane twiddle e^{2 pi i lane k1 / M}
+//   T   shared-memory transpose (XOR-swizzled, conflict-free 16-byte accesses)
+//   F2  in-register DIF DFT-P
+//   F3  radix-2 across lane pairs with half the values exchanged by shuffle.
+// The forward output stays in this "native" per-lane order; the bootstrapping
+// key is stored in the same order, and the inverse is the exact mirror, so no
+// bit-reversal permutation is ever materialised.  tools/fft_model.py replays
+// these index maps in numpy.
+#pragma once
+#include "gw_common.cuh"
+
+namespace gw {
+
+template <int LOGN>
+struct Geo {
+  static constexpr int N = 1 << LOGN;
+  static constexpr int M = N / 2;
+  static constexpr int LOGP = (LOGN - 2) / 2;  // M = 2 P^2
+  static constexpr int P = 1 << LOGP;
+  static constexpr int L = 2 * P;
+  static_assert(2 * P * P == M, "ring dimension must be 4^k * 4 (64, 256, 1024)");
+  static_assert(L <= 32, "one warp per transform");
+  // smem elements (double2) of one P x L tile
+  static constexpr int TILE = P * L;
+};
+
+template <int LOGP>
+__device__ __forceinline__ constexpr int bitrev_c(int x) {
+  int r = 0;
+#pragma unroll
+  for (int k = 0; k < LOGP; ++k) r |= ((x >> k) & 1) << (LOGP - 1 - k);
+  return r;
+}
+
+// multiply by e^{SIGN * 2 pi i t / 64}
+template <int SIGN>
+__device__ __forceinline__ double2 rot64(double2 v, int t) {
+  if (t == 0) return v;
+  if (t == 16) return SIGN > 0 ? make_double2(-v.y, v.x) : make_double2(v.y, -v.x);
+  const double2 w = c_root64[t];
+  return SIGN > 0 ? cmul(v, w) : cmulc(v, w);
+}
+
+// One radix-2 stage of span LEN (compile-time, so every register index folds).
+template <int P, int SIGN, int LEN>
+__device__ __forceinline__ void dif_stage(double2 (&x)[P]) {
+  constexpr int h = LEN / 2;
+#pragma unroll
+  for (int st = 0; st < P; st += LEN) {
+#pragma unroll
+    for (int j = 0; j < h; ++j) {
+      const double2 a = x[st + j], b = x[st + j + h];
+      x[st + j] = cadd(a, b);
+      x[st + j + h] = rot64<SIGN>(csub(a, b), j * (64 / LEN));
+    }
+  }
+}
+
+template <int P, int SIGN, int LEN>
+__device__ __forceinline__ void dit_stage(double2 (&x)[P]) {
+  constexpr int h = LEN / 2;
+#pragma unroll
+  for (int st = 0; st < P; st += LEN) {
+#pragma unroll
+    for (int j = 0; j < h; ++j) {
+      const double2 a = x[st + j];
+      const double2 b = rot64<SIGN>(x[st + j + h], j * (64 / LEN));
+      x[st + j] = cadd(a, b);
+      x[st + j + h] = csub(a, b);
+    }
+  }
+}
+
+// Radix-2 DIF, natural order in, bit-reversed order out, kernel e^{SIGN 2 pi i / P}.
+template <int P, int SIGN, int LEN = P>
+__device__ __forceinline__ void dif(double2 (&x)[P]) {
+  if constexpr (LEN >= 2) {
+    dif_stage<P, SIGN, LEN>(x);
+    dif<P, SIGN, LEN / 2>(x);
+  }
+}
+
+// Radix-2 DIT, bit-reversed order in, natural order out, kernel e^{SIGN 2 pi i / P}.
+template <int P, int SIGN, int LEN = 2>
+__device__ __forceinline__ void dit(double2 (&x)[P]) {
+  if constexpr (LEN <= P) {
+    dit_stage<P, SIGN, LEN>(x);
+    dit<P, SIGN, LEN * 2>(x);
+  }
+}
+
+// Column of the transpose tile holding (row k1, logical column col).
+__device__ __forceinline__ int swz(int k1, int col) { return col ^ ((k1 & 3) << 1); }
+
+// Forward transform.  In: x[m1] = z[L*m1 + l] (l = lane & (L-1)).
+// Out: x[s] = Z[k(l, s)], k = k1 + P*(c + P*d), k1 = l>>1, b = l&1,
+//      c = b*P/2 + s%(P/2), d = s/(P/2).
+// tw1: smem [k1][l] = e^{2 pi i l k1 / M}.  tile: smem scratch of Geo::TILE.
+template <int LOGN>
+__device__ __forceinline__ void fft_forward(double2 (&x)[Geo<LOGN>::P], double2* tile,
+                                            const double2* tw1, int l) {
+  using G = Geo<LOGN>;
+  constexpr int P = G::P, L = G::L, LOGP = G::LOGP;
+  dif<P, +1>(x);  // x[bitrev(k1)]
+#pragma unroll
+  for (int k1 = 1; k1 < P; ++k1) {
+    const int r = bitrev_c<LOGP>(k1);
+    x[r] = cmul(x[r], tw1[k1 * L + l]);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k1 = 0; k1 < P; ++k1) tile[k1 * L + swz(k1, l)] = x[bitrev_c<LOGP>(k1)];
+  __syncwarp();
+  {
+    const int k1 = l >> 1, b = l & 1;
+#pragma unroll
+    for (int a = 0; a < P; ++a) x[a] = tile[k1 * L + swz(k1, b + 2 * a)];
+  }
+  __syncwarp();
+  dif<P, +1>(x);  // x[bitrev(c)] = u_b[c]
+  const bool hi = (l & 1) != 0;
+  double2 y[P];
+#pragma unroll
+  for (int j = 0; j < P / 2; ++j) {
+    const double2 ulo = x[bitrev_c<LOGP>(j)];
+    const double2 uhi = x[bitrev_c<LOGP>(j + P / 2)];
+    const double2 recv = shfl_xor_c(hi ? ulo : uhi, 1);
+    const double2 u0 = hi ? recv : ulo;
+    const double2 u1 = hi ? uhi : recv;
+    // w^c with w = e^{2 pi i / 2P}, c = j + b*P/2  ->  root64[32 j / P (+16)]
+    const double2 w = hi ? c_root64[(32 / P) * j + 16] : c_root64[(32 / P) * j];
+    const double2 t = cmul(u1, w);
+    y[j] = cadd(u0, t);
+    y[j + P / 2] = csub(u0, t);
+  }
+#pragma unroll
+  for (int s = 0; s < P; ++s) x[s] = y[s];
+}
+
+// Inverse transform, exact mirror of fft_forward, scaled by M (no division):
+// In: native layout.  Out: x[m1] = M * z[L*m1 + l].
+template <int LOGN>
+__device__ __forceinline__ void fft_inverse(double2 (&x)[Geo<LOGN>::P], double2* tile,
+                                            const double2* tw1, int l) {
+  using G = Geo<LOGN>;
+  constexpr int P = G::P, L = G::L, LOGP = G::LOGP;
+  const bool hi = (l & 1) != 0;
+  double2 u[P];
+#pragma unroll
+  for (int j = 0; j < P / 2; ++j) {
+    const double2 X0 = x[j], X1 = x[j + P / 2];
+    const double2 S = cadd(X0, X1);
+    const double2 w = hi ? c_root64[(32 / P) * j + 16] : c_root64[(32 / P) * j];
+    const double2 D = cmulc(csub(X0, X1), w);
+    const double2 recv = shfl_xor_c(hi ? S : D, 1);
+    u[bitrev_c<LOGP>(j)] = hi ? recv : S;
+    u[bitrev_c<LOGP>(j + P / 2)] = hi ? D : recv;
+  }
+  dit<P, -1>(u);  // u[a]
+  __syncwarp();
+  {
+    const int k1 = l >> 1, b = l & 1;
+#pragma unroll
+    for (int a = 0; a < P; ++a) tile[k1 * L + swz(k1, b + 2 * a)] = u[a];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k1 = 0; k1 < P; ++k1) x[bitrev_c<LOGP>(k1)] = tile[k1 * L + swz(k1, l)];
+  __syncwarp();
+#pragma unroll
+  for (int k1 = 1; k1 < P; ++k1) {
+    const int r = bitrev_c<LOGP>(k1);
+    x[r] = cmulc(x[r], tw1[k1 * L + l]);
+  }
+  dit<P, -1>(x);  // x[m1]
+}
+
+}  // namespace gw

@@ -1,0 +1,88 @@
+// gates.cuh -- gate prologue / epilogue kernels around the bootstrap.
+//
+// Reference: gatewave/cggi.py:785-854 (`eval_gate_batch`): the per-kind
+// linear combination (_GATE_COMBO, :177-184), the MUX pair (:823-830), and
+// the bootstrap-free kinds NOT (:812-814), COPY (:809-810), CONST (:801-807).
+// Every kernel addresses ciphertext rows through (base, stride) pairs so the
+// same code serves batched operand matrices and the device wire store.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "keyswitch.cuh"
+
+namespace gw {
+
+struct LinJob {        // lin = w0*row(s0) + w1*row(s1) + cmu*mu on the body word
+  int32_t src[2];
+  int32_t w[2];
+  int32_t cmu;
+  int32_t pad;
+};
+
+struct CheapUnit {     // bootstrap-free gate
+  int32_t kind;        // 0 COPY, 1 NOT, 2 CONST0, 3 CONST1
+  int32_t src;
+  int32_t dst;
+  int32_t pad;
+};
+
+__global__ void k_lin(const uint32_t* __restrict__ rows, int64_t stride, const LinJob* __restrict__ jobs,
+                      int J, int W, uint32_t mu, uint32_t* __restrict__ lin, int64_t lin_stride) {
+  const int j = blockIdx.y;
+  if (j >= J) return;
+  const LinJob jb = jobs[j];
+  const uint32_t* r0 = rows + (size_t)jb.src[0] * stride;
+  const uint32_t* r1 = jb.src[1] >= 0 ? rows + (size_t)jb.src[1] * stride : nullptr;
+  uint32_t* dst = lin + (size_t)j * lin_stride;
+  for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < W; col += gridDim.x * blockDim.x) {
+    uint32_t v = (uint32_t)jb.w[0] * r0[col];
+    if (r1) v += (uint32_t)jb.w[1] * r1[col];
+    if (col == W - 1) v += (uint32_t)jb.cmu * mu;
+    dst[col] = v;
+  }
+}
+
+__global__ void k_zero_units(const KsUnit* __restrict__ units, int U, uint32_t* out, int64_t stride, int W) {
+  const int u = blockIdx.y;
+  if (u >= U) return;
+  uint32_t* row = out + (size_t)units[u].out_row * stride;
+  for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < W; col += gridDim.x * blockDim.x) row[col] = 0;
+}
+
+__global__ void k_cheap(const uint32_t* __restrict__ src_rows, int64_t src_stride, const CheapUnit* __restrict__ units,
+                        int C, int W, uint32_t mu, uint32_t* dst_rows, int64_t dst_stride) {
+  const int u = blockIdx.y;
+  if (u >= C) return;
+  const CheapUnit cu = units[u];
+  uint32_t* dst = dst_rows + (size_t)cu.dst * dst_stride;
+  const uint32_t* src = cu.src >= 0 ? src_rows + (size_t)cu.src * src_stride : nullptr;
+  for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < W; col += gridDim.x * blockDim.x) {
+    uint32_t v;
+    switch (cu.kind) {
+      case 0: v = src[col]; break;
+      case 1: v = 0u - src[col]; break;
+      case 2: v = (col == W - 1) ? 0u - mu : 0u; break;
+      default: v = (col == W - 1) ? mu : 0u; break;
+    }
+    dst[col] = v;
+  }
+}
+
+// ext (B, N+1) -> pseudo accumulators (B, 2, N) whose extraction is ext
+// (lets the seam-1 `_keyswitch_kernel` twin reuse the fused kernel).
+__global__ void k_ext_to_acc(const uint32_t* __restrict__ ext, int64_t B, int N, uint32_t* __restrict__ acc) {
+  const int64_t g = blockIdx.y;
+  if (g >= B) return;
+  const uint32_t* e = ext + g * (N + 1);
+  uint32_t* a = acc + g * 2 * N;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < 2 * N; j += gridDim.x * blockDim.x) {
+    uint32_t v = 0;
+    if (j == 0) v = e[0];
+    else if (j < N) v = 0u - e[N - j];
+    else if (j == N) v = e[N];
+    a[j] = v;
+  }
+}
+
+}  // namespace gw

@@ -1,0 +1,961 @@
+// gw_api.cu -- C ABI of the B200 CGGI engine (include/gatewave_b200.h).
+//
+// Host-side responsibilities: parameter envelope, key upload + on-device FFT
+// pre-transform, scratch management, descriptor building for gate batches
+// and level plans, and the launch sequence per level:
+//   k_lin -> k_blind_rotate -> k_zero_units -> k_keyswitch -> k_cheap
+// All launches go to the context stream; only the host-pointer entry points
+// synchronise (they must hand results back to the caller).
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/gatewave_b200.h"
+#include "blind_rotate.cuh"
+#include "gates.cuh"
+#include "keyswitch.cuh"
+
+using namespace gw;
+
+struct BatchDesc {
+  void* mem = nullptr;
+  LinJob* jobs = nullptr;
+  KsUnit* units = nullptr;
+  CheapUnit* cheap = nullptr;
+  int J = 0, U = 0, C = 0;
+};
+
+struct gw_ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  gw_params p{};
+  bool have_params = false;
+  bool have_keys = false;   // both keys present
+  bool have_bk = false;
+  bool have_ksk = false;
+  int logn = 0;
+  int Wp = 0;  // padded LWE row stride (words)
+  // keys
+  double2* bk_fft = nullptr;
+  size_t bk_fft_count = 0;
+  uint32_t* ksk = nullptr;
+  double2* tables = nullptr;
+  uint32_t* tv_dev = nullptr;  // default test vector (0 | mu)
+  // scratch
+  uint32_t* lin = nullptr;
+  size_t lin_cap = 0;  // rows
+  uint32_t* acc = nullptr;
+  size_t acc_cap = 0;  // rows (jobs)
+  uint32_t* io = nullptr;
+  size_t io_cap = 0;  // words
+  void* desc = nullptr;
+  size_t desc_cap = 0;  // bytes
+  void* desc_host = nullptr;  // pinned
+  size_t desc_host_cap = 0;
+  // wire store
+  uint32_t* wires = nullptr;
+  int64_t wire_slots = 0;
+  // device descriptors of homogeneous gate batches, keyed by (opcode, B)
+  std::map<uint64_t, BatchDesc> batch_desc;
+  // timing / accounting
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int64_t launches = 0;
+  std::string err;
+};
+
+struct gw_plan {
+  int64_t n_levels = 0;
+  std::vector<int> J, U, C;            // per level counts
+  std::vector<size_t> job_off, unit_off, cheap_off;
+  LinJob* jobs = nullptr;
+  KsUnit* units = nullptr;
+  CheapUnit* cheap = nullptr;
+  int max_jobs = 0;
+};
+
+namespace {
+
+int fail(gw_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+#define GW_CUDA(ctx, expr)                                                             \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail((ctx), GW_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define GW_LAUNCHED(ctx)                                                               \
+  do {                                                                                 \
+    (ctx)->launches++;                                                                 \
+    cudaError_t e_ = cudaGetLastError();                                               \
+    if (e_ != cudaSuccess)                                                             \
+      return fail((ctx), GW_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+int ilog2(int v) {
+  int r = 0;
+  while ((1 << r) < v) ++r;
+  return (1 << r) == v ? r : -1;
+}
+
+template <typename T>
+int ensure(gw_ctx* c, T** ptr, size_t* cap, size_t need, size_t elem_bytes) {
+  if (*cap >= need && *ptr) return GW_OK;
+  if (*ptr) {
+    GW_CUDA(c, cudaStreamSynchronize(c->stream));  // in-flight work may still use it
+    cudaFree(*ptr);
+  }
+  *ptr = nullptr;
+  *cap = 0;
+  size_t n = need < 16 ? 16 : need;
+  n += n / 4;
+  GW_CUDA(c, cudaMalloc((void**)ptr, n * elem_bytes));
+  *cap = n;
+  return GW_OK;
+}
+
+int ensure_desc(gw_ctx* c, size_t bytes) {
+  if (c->desc_cap < bytes || !c->desc) {
+    if (c->desc) cudaFree(c->desc);
+    c->desc = nullptr;
+    size_t n = bytes + bytes / 4 + 256;
+    GW_CUDA(c, cudaMalloc(&c->desc, n));
+    c->desc_cap = n;
+  }
+  if (c->desc_host_cap < bytes || !c->desc_host) {
+    // the previous contents may still be in flight
+    GW_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (c->desc_host) cudaFreeHost(c->desc_host);
+    c->desc_host = nullptr;
+    size_t n = bytes + bytes / 4 + 256;
+    GW_CUDA(c, cudaMallocHost(&c->desc_host, n));
+    c->desc_host_cap = n;
+  }
+  return GW_OK;
+}
+
+// Host twiddle tables, long double -> correctly rounded-ish doubles.
+void host_tables(int logn, std::vector<double2>& out) {
+  const int N = 1 << logn, M = N / 2;
+  const int P = 1 << ((logn - 2) / 2), L = 2 * P;
+  out.resize(2 * P * L);
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (int k1 = 0; k1 < P; ++k1)
+    for (int l = 0; l < L; ++l) {
+      long double a = 2.0L * pi * (long double)(l * k1) / (long double)M;
+      out[k1 * L + l] = make_double2((double)cosl(a), (double)sinl(a));
+    }
+  for (int m1 = 0; m1 < P; ++m1)
+    for (int l = 0; l < L; ++l) {
+      long double a = pi * (long double)(L * m1 + l) / (long double)N;
+      out[P * L + m1 * L + l] = make_double2((double)cosl(a), (double)sinl(a));
+    }
+}
+
+int upload_roots(gw_ctx* c) {
+  double2 roots[64];
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (int t = 0; t < 64; ++t) {
+    long double a = 2.0L * pi * (long double)t / 64.0L;
+    roots[t] = make_double2((double)cosl(a), (double)sinl(a));
+  }
+  // exact values where they exist
+  roots[0] = make_double2(1.0, 0.0);
+  roots[16] = make_double2(0.0, 1.0);
+  roots[32] = make_double2(-1.0, 0.0);
+  roots[48] = make_double2(0.0, -1.0);
+  GW_CUDA(c, cudaMemcpyToSymbol(c_root64, roots, sizeof(roots)));
+  return GW_OK;
+}
+
+// ---- kernel dispatch over (LOGN, LEV) --------------------------------------
+
+template <int LOGN, int LEV>
+int launch_br_t(gw_ctx* c, const BrArgs& a0) {
+  BrArgs a = a0;
+  int gc = (int)((a.B + c->sm_count - 1) / c->sm_count);
+  if (gc < 1) gc = 1;
+  if (gc > 4) gc = 4;
+  int max_smem = 0;
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+  while (gc > 1 && BrSmem<LOGN, LEV>::bytes(gc, a.n) > (size_t)max_smem) --gc;
+  const size_t smem = BrSmem<LOGN, LEV>::bytes(gc, a.n);
+  if (smem > (size_t)max_smem)
+    return fail(c, GW_ERR_PARAM, "LWE dimension too large for the on-chip blind rotation");
+  GW_CUDA(c, cudaFuncSetAttribute(k_blind_rotate<LOGN, LEV>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  a.gates_per_cta = gc;
+  const int grid = (a.B + gc - 1) / gc;
+  k_blind_rotate<LOGN, LEV><<<grid, 64 * gc, smem, c->stream>>>(a);
+  GW_LAUNCHED(c);
+  return GW_OK;
+}
+
+template <int LOGN>
+int launch_br_n(gw_ctx* c, const BrArgs& a) {
+  switch (c->p.l) {
+    case 1: return launch_br_t<LOGN, 1>(c, a);
+    case 2: return launch_br_t<LOGN, 2>(c, a);
+    case 3: return launch_br_t<LOGN, 3>(c, a);
+  }
+  return fail(c, GW_ERR_PARAM, "gadget levels outside 1..3");
+}
+
+int launch_br(gw_ctx* c, const BrArgs& a) {
+  switch (c->logn) {
+    case 6: return launch_br_n<6>(c, a);
+    case 8: return launch_br_n<8>(c, a);
+    case 10: return launch_br_n<10>(c, a);
+  }
+  return fail(c, GW_ERR_PARAM, "ring dimension not supported");
+}
+
+template <int LOGN, int LEV>
+int launch_bk_t(gw_ctx* c, const uint32_t* bk_dev) {
+  const long long jobs = (long long)c->p.n * 2 * LEV * 4;
+  const int grid = (int)((jobs + 3) / 4);
+  k_bk_to_fft<LOGN, LEV><<<grid, 128, 0, c->stream>>>(bk_dev, c->p.n, c->tables, c->bk_fft);
+  GW_LAUNCHED(c);
+  return GW_OK;
+}
+
+template <int LOGN>
+int launch_bk_n(gw_ctx* c, const uint32_t* bk) {
+  switch (c->p.l) {
+    case 1: return launch_bk_t<LOGN, 1>(c, bk);
+    case 2: return launch_bk_t<LOGN, 2>(c, bk);
+    case 3: return launch_bk_t<LOGN, 3>(c, bk);
+  }
+  return fail(c, GW_ERR_PARAM, "gadget levels outside 1..3");
+}
+
+int launch_bk(gw_ctx* c, const uint32_t* bk) {
+  switch (c->logn) {
+    case 6: return launch_bk_n<6>(c, bk);
+    case 8: return launch_bk_n<8>(c, bk);
+    case 10: return launch_bk_n<10>(c, bk);
+  }
+  return fail(c, GW_ERR_PARAM, "ring dimension not supported");
+}
+
+constexpr int KS_GT = 16;
+
+int launch_ks(gw_ctx* c, const uint32_t* acc, const KsUnit* units, int U, uint32_t* out, int64_t out_stride) {
+  if (U <= 0) return GW_OK;
+  const int N = c->p.N, W = c->p.n + 1;
+  {
+    dim3 grid((W + 255) / 256, U);
+    k_zero_units<<<grid, 256, 0, c->stream>>>(units, U, out, out_stride, W);
+    GW_LAUNCHED(c);
+  }
+  KsArgs a;
+  a.acc = acc;
+  a.units = units;
+  a.count = U;
+  a.ksk = c->ksk;
+  a.N = N;
+  a.t = c->p.ks_levels;
+  a.gamma = c->p.ks_base_bits;
+  a.W = W;
+  a.Wp = c->Wp;
+  a.chunk = N < 64 ? N : 64;
+  a.out = out;
+  a.out_stride = out_stride;
+  const int threads = ((c->Wp / 4) + 31) / 32 * 32;
+  if (threads > 160) return fail(c, GW_ERR_PARAM, "LWE dimension too large for the keyswitch tile");
+  dim3 grid((U + KS_GT - 1) / KS_GT, (N + a.chunk - 1) / a.chunk);
+  const size_t smem = sizeof(uint32_t) * KS_GT * a.chunk;
+  const int V = (1 << a.gamma) - 1;
+  if (V == 3) k_keyswitch<KS_GT, 3><<<grid, threads, smem, c->stream>>>(a);
+  else if (V == 1) k_keyswitch<KS_GT, 1><<<grid, threads, smem, c->stream>>>(a);
+  else k_keyswitch<KS_GT, 0><<<grid, threads, smem, c->stream>>>(a);
+  GW_LAUNCHED(c);
+  return GW_OK;
+}
+
+int launch_lin(gw_ctx* c, const uint32_t* rows, int64_t stride, const LinJob* jobs, int J) {
+  if (J <= 0) return GW_OK;
+  const int W = c->p.n + 1;
+  dim3 grid((W + 255) / 256, J);
+  k_lin<<<grid, 256, 0, c->stream>>>(rows, stride, jobs, J, W, c->p.mu, c->lin, c->Wp);
+  GW_LAUNCHED(c);
+  return GW_OK;
+}
+
+int launch_cheap(gw_ctx* c, const uint32_t* src, int64_t src_stride, const CheapUnit* units, int C,
+                 uint32_t* dst, int64_t dst_stride) {
+  if (C <= 0) return GW_OK;
+  const int W = c->p.n + 1;
+  dim3 grid((W + 255) / 256, C);
+  k_cheap<<<grid, 256, 0, c->stream>>>(src, src_stride, units, C, W, c->p.mu, dst, dst_stride);
+  GW_LAUNCHED(c);
+  return GW_OK;
+}
+
+int ready(gw_ctx* c, bool need_bk = true, bool need_ksk = true) {
+  if (!c) return GW_ERR_ARG;
+  if (!c->have_params) return fail(c, GW_ERR_STATE, "parameters not set");
+  if (need_bk && !c->have_bk) return fail(c, GW_ERR_STATE, "bootstrapping key not uploaded");
+  if (need_ksk && !c->have_ksk) return fail(c, GW_ERR_STATE, "keyswitch key not uploaded");
+  return GW_OK;
+}
+
+// One level over a row space: jobs/units/cheap are DEVICE descriptor arrays.
+int run_level(gw_ctx* c, const uint32_t* src, int64_t src_stride, uint32_t* dst, int64_t dst_stride,
+              const LinJob* jobs, int J, const KsUnit* units, int U, const CheapUnit* cheap, int C) {
+  int rc;
+  if (J > 0) {
+    if ((rc = ensure(c, &c->lin, &c->lin_cap, (size_t)J * c->Wp, sizeof(uint32_t)))) return rc;
+    if ((rc = ensure(c, &c->acc, &c->acc_cap, (size_t)J * 2 * c->p.N, sizeof(uint32_t)))) return rc;
+    if ((rc = launch_lin(c, src, src_stride, jobs, J))) return rc;
+    BrArgs a;
+    a.lin = c->lin;
+    a.lin_stride = c->Wp;
+    a.B = J;
+    a.n = c->p.n;
+    a.tv = c->tv_dev;
+    a.bk = c->bk_fft;
+    a.tables = c->tables;
+    a.acc_out = c->acc;
+    a.bg_bits = c->p.bg_bits;
+    uint64_t off = 1ull << (32 - c->p.l * c->p.bg_bits - 1);
+    for (int j = 1; j <= c->p.l; ++j) off += (uint64_t)(1u << (c->p.bg_bits - 1)) << (32 - j * c->p.bg_bits);
+    a.offs = (uint32_t)(off & 0xFFFFFFFFull);
+    a.gates_per_cta = 1;
+    if ((rc = launch_br(c, a))) return rc;
+    if ((rc = launch_ks(c, c->acc, units, U, dst, dst_stride))) return rc;
+  }
+  if ((rc = launch_cheap(c, src, src_stride, cheap, C, dst, dst_stride))) return rc;
+  return GW_OK;
+}
+
+// Host-side descriptors for one gate (cggi.py:816-852 semantics).
+void describe_gate(int op, int32_t s0, int32_t s1, int32_t s2, int32_t out, uint32_t mu,
+                   std::vector<LinJob>& jobs, std::vector<KsUnit>& units, std::vector<CheapUnit>& cheap) {
+  static const int combo[6][3] = {{-1, 1, 1}, {1, 1, 1}, {1, -1, -1}, {-1, -1, -1}, {2, 2, 2}, {-2, -2, -2}};
+  if (op <= GW_XNOR) {
+    LinJob j{};
+    j.src[0] = s0; j.src[1] = s1;
+    j.w[0] = combo[op][1]; j.w[1] = combo[op][2];
+    j.cmu = combo[op][0];
+    const int idx = (int)jobs.size();
+    jobs.push_back(j);
+    units.push_back(KsUnit{idx, -1, out, 0u});
+  } else if (op == GW_BOOTSTRAP) {
+    LinJob j{};
+    j.src[0] = s0; j.src[1] = -1; j.w[0] = 1; j.w[1] = 0; j.cmu = 0;
+    const int idx = (int)jobs.size();
+    jobs.push_back(j);
+    units.push_back(KsUnit{idx, -1, out, 0u});
+  } else if (op == GW_MUX) {
+    LinJob j1{}, j2{};
+    j1.src[0] = s0; j1.src[1] = s1; j1.w[0] = 1; j1.w[1] = 1; j1.cmu = -1;   // sel + a - mu
+    j2.src[0] = s2; j2.src[1] = s0; j2.w[0] = 1; j2.w[1] = -1; j2.cmu = -1;  // b - sel - mu
+    const int idx = (int)jobs.size();
+    jobs.push_back(j1);
+    jobs.push_back(j2);
+    units.push_back(KsUnit{idx, idx + 1, out, mu});  // pre.b += mu (cggi.py:845)
+  } else {
+    CheapUnit u{};
+    u.kind = op == GW_COPY ? 0 : op == GW_NOT ? 1 : op == GW_CONST0 ? 2 : 3;
+    u.src = s0;
+    u.dst = out;
+    cheap.push_back(u);
+  }
+}
+
+int arity_of(int op) {
+  if (op <= GW_XNOR) return 2;
+  if (op == GW_NOT || op == GW_COPY || op == GW_BOOTSTRAP) return 1;
+  if (op == GW_MUX) return 3;
+  if (op == GW_CONST0 || op == GW_CONST1) return 0;
+  return -1;
+}
+
+// Upload host descriptor vectors into the device descriptor arena.
+int upload_desc(gw_ctx* c, const std::vector<LinJob>& jobs, const std::vector<KsUnit>& units,
+                const std::vector<CheapUnit>& cheap, LinJob** dj, KsUnit** du, CheapUnit** dc) {
+  const size_t bj = jobs.size() * sizeof(LinJob), bu = units.size() * sizeof(KsUnit),
+               bc = cheap.size() * sizeof(CheapUnit);
+  const size_t total = bj + bu + bc;
+  int rc;
+  // the pinned staging buffer may still feed an earlier async copy
+  GW_CUDA(c, cudaStreamSynchronize(c->stream));
+  if ((rc = ensure_desc(c, total))) return rc;
+  char* h = (char*)c->desc_host;
+  if (bj) memcpy(h, jobs.data(), bj);
+  if (bu) memcpy(h + bj, units.data(), bu);
+  if (bc) memcpy(h + bj + bu, cheap.data(), bc);
+  GW_CUDA(c, cudaMemcpyAsync(c->desc, h, total, cudaMemcpyHostToDevice, c->stream));
+  char* d = (char*)c->desc;
+  *dj = (LinJob*)d;
+  *du = (KsUnit*)(d + bj);
+  *dc = (CheapUnit*)(d + bj + bu);
+  return GW_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+int gw_version(void) { return 1; }
+
+int gw_device_count(int* count) {
+  if (!count) return GW_ERR_ARG;
+  if (cudaGetDeviceCount(count) != cudaSuccess) {
+    *count = 0;
+    cudaGetLastError();
+  }
+  return GW_OK;
+}
+
+int gw_create(int device, gw_ctx** out) {
+  if (!out) return GW_ERR_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return GW_ERR_CUDA;
+  }
+  if (device < 0 || device >= ndev) return GW_ERR_ARG;
+  gw_ctx* c = new gw_ctx();
+  c->device = device;
+  int rc = GW_OK;
+  if (cudaSetDevice(device) != cudaSuccess) rc = GW_ERR_CUDA;
+  if (!rc && cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) rc = GW_ERR_CUDA;
+  c->own_stream = true;
+  if (!rc) cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (!rc && (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess)) rc = GW_ERR_CUDA;
+  if (!rc) rc = upload_roots(c);
+  if (rc) {
+    gw_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return GW_OK;
+}
+
+int gw_destroy(gw_ctx* c) {
+  if (!c) return GW_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  cudaFree(c->bk_fft);
+  cudaFree(c->ksk);
+  cudaFree(c->tables);
+  cudaFree(c->tv_dev);
+  cudaFree(c->lin);
+  cudaFree(c->acc);
+  cudaFree(c->io);
+  cudaFree(c->desc);
+  cudaFree(c->wires);
+  for (auto& kv : c->batch_desc) cudaFree(kv.second.mem);
+  if (c->desc_host) cudaFreeHost(c->desc_host);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return GW_OK;
+}
+
+const char* gw_last_error(const gw_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int gw_set_stream(gw_ctx* c, void* s) {
+  if (!c) return GW_ERR_ARG;
+  cudaSetDevice(c->device);
+  if (c->stream) GW_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  if (s) {
+    c->stream = (cudaStream_t)s;
+    c->own_stream = false;
+  } else {
+    GW_CUDA(c, cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  return GW_OK;
+}
+
+int gw_sync(gw_ctx* c) {
+  if (!c) return GW_ERR_ARG;
+  GW_CUDA(c, cudaStreamSynchronize(c->stream));
+  return GW_OK;
+}
+
+int gw_set_params(gw_ctx* c, const gw_params* p) {
+  if (!c || !p) return GW_ERR_ARG;
+  // ParamSet.__post_init__ (cggi.py:86-110)
+  if (p->n < 1) return fail(c, GW_ERR_PARAM, "LWE dimension must be positive");
+  if (p->N < 2 || (p->N & (p->N - 1))) return fail(c, GW_ERR_PARAM, "ring dimension must be a power of two >= 2");
+  if (!(p->bg_bits >= 1 && p->l >= 1 && p->l * p->bg_bits <= 32))
+    return fail(c, GW_ERR_PARAM, "gadget levels * base bits must fit 32 bits");
+  const int logn = ilog2(p->N);
+  if (logn + p->bg_bits > 32) return fail(c, GW_ERR_PARAM, "gadget digits too wide for exact convolution");
+  if (!(p->ks_base_bits >= 1 && p->ks_levels >= 1 && p->ks_levels * p->ks_base_bits <= 32))
+    return fail(c, GW_ERR_PARAM, "keyswitch levels * base bits must fit 32 bits");
+  if (p->mu == 0) return fail(c, GW_ERR_PARAM, "mu must be a nonzero uint32");
+  // Engine envelope: warp-FFT geometry and FP64 exactness.
+  if (!(logn == 6 || logn == 8 || logn == 10))
+    return fail(c, GW_ERR_PARAM, "ring dimension not supported by the B200 engine (64, 256, 1024)");
+  if (p->l > 3) return fail(c, GW_ERR_PARAM, "gadget levels > 3 not supported by the B200 engine");
+  if (p->bg_bits > 16) return fail(c, GW_ERR_PARAM, "gadget base > 2^16 not supported by the B200 engine");
+  // |coefficient| <= 2l * N * 2^(Bg-1) * 2^15 must stay <= 2^40 for the FFT bound
+  if (std::log2(2.0 * p->l) + logn + (p->bg_bits - 1) + 15 > 40.0)
+    return fail(c, GW_ERR_PARAM, "parameters outside the exact FP64 convolution envelope");
+  if (p->ks_levels * p->ks_base_bits > 31)
+    return fail(c, GW_ERR_PARAM, "keyswitch precision t*gamma > 31 not supported by the B200 engine");
+  if (((p->n + 1 + 3) / 4) > 160) return fail(c, GW_ERR_PARAM, "LWE dimension > 639 not supported by the B200 engine");
+  const bool same = c->have_params && memcmp(&c->p, p, sizeof(gw_params)) == 0;
+  c->p = *p;
+  c->logn = logn;
+  c->Wp = (p->n + 1 + 3) & ~3;
+  c->have_params = true;
+  if (!same) c->have_keys = c->have_bk = c->have_ksk = false;
+  cudaSetDevice(c->device);
+  // tables + default test vector (cggi.py:712-713: a = 0, b = mu)
+  std::vector<double2> t;
+  host_tables(logn, t);
+  cudaFree(c->tables);
+  c->tables = nullptr;
+  GW_CUDA(c, cudaMalloc(&c->tables, t.size() * sizeof(double2)));
+  GW_CUDA(c, cudaMemcpy(c->tables, t.data(), t.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  std::vector<uint32_t> tv(2 * p->N, 0u);
+  for (int j = 0; j < p->N; ++j) tv[p->N + j] = p->mu;
+  cudaFree(c->tv_dev);
+  c->tv_dev = nullptr;
+  GW_CUDA(c, cudaMalloc(&c->tv_dev, tv.size() * sizeof(uint32_t)));
+  GW_CUDA(c, cudaMemcpy(c->tv_dev, tv.data(), tv.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  return GW_OK;
+}
+
+int gw_upload_keys(gw_ctx* c, const uint32_t* bk_coeff, const uint32_t* ksk) {
+  if (!c || (!bk_coeff && !ksk)) return GW_ERR_ARG;
+  if (!c->have_params) return fail(c, GW_ERR_STATE, "parameters not set");
+  cudaSetDevice(c->device);
+  const int n = c->p.n, N = c->p.N, l = c->p.l, t = c->p.ks_levels, V = (1 << c->p.ks_base_bits) - 1;
+  GW_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (bk_coeff) {
+    c->have_bk = false;
+    const size_t bk_words = (size_t)n * 2 * l * 2 * N;
+    // bootstrapping key: upload coefficient domain, transform on device
+    uint32_t* bk_dev = nullptr;
+    GW_CUDA(c, cudaMalloc(&bk_dev, bk_words * sizeof(uint32_t)));
+    cudaError_t e = cudaMemcpyAsync(bk_dev, bk_coeff, bk_words * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream);
+    if (e != cudaSuccess) {
+      cudaFree(bk_dev);
+      return fail(c, GW_ERR_CUDA, cudaGetErrorString(e));
+    }
+    const size_t nfft = (size_t)n * 2 * (2 * l) * 2 * (N / 2);
+    if (c->bk_fft_count != nfft) {
+      cudaFree(c->bk_fft);
+      c->bk_fft = nullptr;
+      c->bk_fft_count = 0;
+      e = cudaMalloc(&c->bk_fft, nfft * sizeof(double2));
+      if (e != cudaSuccess) {
+        cudaFree(bk_dev);
+        return fail(c, GW_ERR_CUDA, cudaGetErrorString(e));
+      }
+      c->bk_fft_count = nfft;
+    }
+    int rc = launch_bk(c, bk_dev);
+    cudaError_t es = cudaStreamSynchronize(c->stream);
+    cudaFree(bk_dev);
+    if (rc) return rc;
+    if (es != cudaSuccess) return fail(c, GW_ERR_CUDA, cudaGetErrorString(es));
+    c->have_bk = true;
+  }
+  if (ksk) {
+    c->have_ksk = false;
+    // keyswitch key: (N, t, V, n+1) -> padded rows of Wp words
+    const size_t rows = (size_t)N * t * V;
+    cudaFree(c->ksk);
+    c->ksk = nullptr;
+    GW_CUDA(c, cudaMalloc(&c->ksk, rows * c->Wp * sizeof(uint32_t)));
+    GW_CUDA(c, cudaMemsetAsync(c->ksk, 0, rows * c->Wp * sizeof(uint32_t), c->stream));
+    GW_CUDA(c, cudaMemcpy2DAsync(c->ksk, c->Wp * sizeof(uint32_t), ksk, (n + 1) * sizeof(uint32_t),
+                                 (n + 1) * sizeof(uint32_t), rows, cudaMemcpyHostToDevice, c->stream));
+    GW_CUDA(c, cudaStreamSynchronize(c->stream));
+    c->have_ksk = true;
+  }
+  c->have_keys = c->have_bk && c->have_ksk;
+  return GW_OK;
+}
+
+int gw_bk_fft_size(gw_ctx* c, int64_t* n_complex) {
+  if (!c || !n_complex) return GW_ERR_ARG;
+  if (!c->have_bk) return fail(c, GW_ERR_STATE, "bootstrapping key not uploaded");
+  *n_complex = (int64_t)c->bk_fft_count;
+  return GW_OK;
+}
+
+int gw_download_bk_fft(gw_ctx* c, double* out) {
+  if (!c || !out) return GW_ERR_ARG;
+  if (!c->have_bk) return fail(c, GW_ERR_STATE, "bootstrapping key not uploaded");
+  cudaSetDevice(c->device);
+  GW_CUDA(c, cudaMemcpyAsync(out, c->bk_fft, c->bk_fft_count * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
+  GW_CUDA(c, cudaStreamSynchronize(c->stream));
+  return GW_OK;
+}
+
+int gw_blind_rotate(gw_ctx* c, const uint32_t* lin, int64_t B, const uint32_t* tv, uint32_t* acc) {
+  int rc = ready(c, true, false);
+  if (rc) return rc;
+  if (B < 0 || (B > 0 && (!lin || !tv || !acc))) return fail(c, GW_ERR_ARG, "null buffer");
+  if (B == 0) return GW_OK;
+  if (B > (1 << 30)) return fail(c, GW_ERR_ARG, "batch too large");
+  cudaSetDevice(c->device);
+  const int n = c->p.n, N = c->p.N;
+  // io: lin rows (Wp stride) + tv
+  const size_t need = (size_t)B * c->Wp + 2 * N;
+  if ((rc = ensure(c, &c->io, &c->io_cap, need, sizeof(uint32_t)))) return rc;
+  if ((rc = ensure(c, &c->acc, &c->acc_cap, (size_t)B * 2 * N, sizeof(uint32_t)))) return rc;
+  uint32_t* dlin = c->io;
+  uint32_t* dtv = c->io + (size_t)B * c->Wp;
+  GW_CUDA(c, cudaMemcpy2DAsync(dlin, c->Wp * sizeof(uint32_t), lin, (n + 1) * sizeof(uint32_t),
+                               (n + 1) * sizeof(uint32_t), B, cudaMemcpyHostToDevice, c->stream));
+  GW_CUDA(c, cudaMemcpyAsync(dtv, tv, 2 * N * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+  BrArgs a;
+  a.lin = dlin;
+  a.lin_stride = c->Wp;
+  a.B = (int)B;
+  a.n = n;
+  a.tv = dtv;
+  a.bk = c->bk_fft;
+  a.tables = c->tables;
+  a.acc_out = c->acc;
+  a.bg_bits = c->p.bg_bits;
+  uint64_t off = 1ull << (32 - c->p.l * c->p.bg_bits - 1);
+  for (int j = 1; j <= c->p.l; ++j) off += (uint64_t)(1u << (c->p.bg_bits - 1)) << (32 - j * c->p.bg_bits);
+  a.offs = (uint32_t)(off & 0xFFFFFFFFull);
+  a.gates_per_cta = 1;
+  if ((rc = launch_br(c, a))) return rc;
+  GW_CUDA(c, cudaMemcpyAsync(acc, c->acc, (size_t)B * 2 * N * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+  GW_CUDA(c, cudaStreamSynchronize(c->stream));
+  return GW_OK;
+}
+
+int gw_keyswitch(gw_ctx* c, const uint32_t* ext, int64_t B, uint32_t* out) {
+  int rc = ready(c, false, true);
+  if (rc) return rc;
+  if (B < 0 || (B > 0 && (!ext || !out))) return fail(c, GW_ERR_ARG, "null buffer");
+  if (B == 0) return GW_OK;
+  cudaSetDevice(c->device);
+  const int N = c->p.N, W = c->p.n + 1;
+  const size_t ext_words = (size_t)B * (N + 1);
+  const size_t need = ext_words + (size_t)B * c->Wp;
+  if ((rc = ensure(c, &c->io, &c->io_cap, need, sizeof(uint32_t)))) return rc;
+  if ((rc = ensure(c, &c->acc, &c->acc_cap, (size_t)B * 2 * N, sizeof(uint32_t)))) return rc;
+  uint32_t* dext = c->io;
+  uint32_t* dout = c->io + ext_words;
+  GW_CUDA(c, cudaMemcpyAsync(dext, ext, ext_words * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+  {
+    dim3 grid((2 * N + 255) / 256, (unsigned)B);
+    k_ext_to_acc<<<grid, 256, 0, c->stream>>>(dext, B, N, c->acc);
+    GW_LAUNCHED(c);
+  }
+  std::vector<LinJob> jobs;
+  std::vector<KsUnit> units((size_t)B);
+  std::vector<CheapUnit> cheap;
+  for (int64_t g = 0; g < B; ++g) units[g] = KsUnit{(int32_t)g, -1, (int32_t)g, 0u};
+  LinJob* dj;
+  KsUnit* du;
+  CheapUnit* dc;
+  if ((rc = upload_desc(c, jobs, units, cheap, &dj, &du, &dc))) return rc;
+  if ((rc = launch_ks(c, c->acc, du, (int)B, dout, c->Wp))) return rc;
+  GW_CUDA(c, cudaMemcpy2DAsync(out, W * sizeof(uint32_t), dout, c->Wp * sizeof(uint32_t), W * sizeof(uint32_t), B,
+                               cudaMemcpyDeviceToHost, c->stream));
+  GW_CUDA(c, cudaStreamSynchronize(c->stream));
+  return GW_OK;
+}
+
+static int eval_stacked(gw_ctx* c, int opcode, const uint32_t* stacked, int arity, int64_t B, uint32_t* d_out,
+                        int64_t out_stride) {
+  // Descriptors of a homogeneous batch depend only on (opcode, B): cache them
+  // on the device so repeated batches enqueue without any host round trip.
+  const uint64_t key = ((uint64_t)opcode << 40) | (uint64_t)B;
+  auto it = c->batch_desc.find(key);
+  if (it == c->batch_desc.end()) {
+    std::vector<LinJob> jobs;
+    std::vector<KsUnit> units;
+    std::vector<CheapUnit> cheap;
+    for (int64_t g = 0; g < B; ++g) {
+      const int32_t s0 = arity > 0 ? (int32_t)g : -1;
+      const int32_t s1 = arity > 1 ? (int32_t)(B + g) : -1;
+      const int32_t s2 = arity > 2 ? (int32_t)(2 * B + g) : -1;
+      describe_gate(opcode, s0, s1, s2, (int32_t)g, c->p.mu, jobs, units, cheap);
+    }
+    BatchDesc d;
+    d.J = (int)jobs.size();
+    d.U = (int)units.size();
+    d.C = (int)cheap.size();
+    const size_t bj = jobs.size() * sizeof(LinJob), bu = units.size() * sizeof(KsUnit),
+                 bc = cheap.size() * sizeof(CheapUnit);
+    GW_CUDA(c, cudaMalloc(&d.mem, bj + bu + bc + 16));
+    char* m = (char*)d.mem;
+    if (bj) GW_CUDA(c, cudaMemcpy(m, jobs.data(), bj, cudaMemcpyHostToDevice));
+    if (bu) GW_CUDA(c, cudaMemcpy(m + bj, units.data(), bu, cudaMemcpyHostToDevice));
+    if (bc) GW_CUDA(c, cudaMemcpy(m + bj + bu, cheap.data(), bc, cudaMemcpyHostToDevice));
+    d.jobs = (LinJob*)m;
+    d.units = (KsUnit*)(m + bj);
+    d.cheap = (CheapUnit*)(m + bj + bu);
+    if (c->batch_desc.size() > 64) {
+      GW_CUDA(c, cudaStreamSynchronize(c->stream));
+      for (auto& kv : c->batch_desc) cudaFree(kv.second.mem);
+      c->batch_desc.clear();
+    }
+    it = c->batch_desc.emplace(key, d).first;
+  }
+  const BatchDesc& d = it->second;
+  return run_level(c, stacked, c->Wp, d_out, out_stride, d.jobs, d.J, d.units, d.U, d.cheap, d.C);
+}
+
+static int check_batch(gw_ctx* c, int opcode, int arity, int64_t B) {
+  int rc = ready(c);
+  if (rc) return rc;
+  const int want = arity_of(opcode);
+  if (want < 0) return fail(c, GW_ERR_ARG, "unknown opcode");
+  if (arity != want) return fail(c, GW_ERR_DIM, "operand count does not match the gate arity");
+  if (B < 0 || B > (1 << 26)) return fail(c, GW_ERR_ARG, "bad batch size");
+  return GW_OK;
+}
+
+int gw_eval_gate_batch_device(gw_ctx* c, int opcode, const uint32_t* const* d_ops, int64_t in_stride, int arity,
+                              int64_t B, uint32_t* d_out, int64_t out_stride) {
+  int rc = check_batch(c, opcode, arity, B);
+  if (rc) return rc;
+  if (B == 0) return GW_OK;
+  for (int k = 0; k < arity; ++k)
+    if (!d_ops[k]) return fail(c, GW_ERR_ARG, "null operand");
+  if (!d_out) return fail(c, GW_ERR_ARG, "null output");
+  cudaSetDevice(c->device);
+  const int W = c->p.n + 1;
+  const uint32_t* stacked = nullptr;
+  if (arity > 0) {
+    // operands that already form one stacked (arity*B, Wp) block are used in place
+    bool inplace = in_stride == c->Wp;
+    for (int k = 1; k < arity && inplace; ++k) inplace = d_ops[k] == d_ops[0] + (size_t)k * B * c->Wp;
+    if (inplace) {
+      stacked = d_ops[0];
+    } else {
+      if ((rc = ensure(c, &c->io, &c->io_cap, (size_t)arity * B * c->Wp, sizeof(uint32_t)))) return rc;
+      for (int k = 0; k < arity; ++k)
+        GW_CUDA(c, cudaMemcpy2DAsync(c->io + (size_t)k * B * c->Wp, c->Wp * sizeof(uint32_t), d_ops[k],
+                                     in_stride * sizeof(uint32_t), W * sizeof(uint32_t), B, cudaMemcpyDeviceToDevice,
+                                     c->stream));
+      stacked = c->io;
+    }
+  }
+  return eval_stacked(c, opcode, stacked, arity, B, d_out, out_stride);
+}
+
+int gw_eval_gate_batch(gw_ctx* c, int opcode, const uint32_t* const* ops, int arity, int64_t B, uint32_t* out) {
+  int rc = check_batch(c, opcode, arity, B);
+  if (rc) return rc;
+  if (B == 0) return GW_OK;
+  for (int k = 0; k < arity; ++k)
+    if (!ops[k]) return fail(c, GW_ERR_ARG, "null operand");
+  if (!out) return fail(c, GW_ERR_ARG, "null output");
+  cudaSetDevice(c->device);
+  const int W = c->p.n + 1;
+  const size_t in_words = (size_t)arity * B * c->Wp;
+  if ((rc = ensure(c, &c->io, &c->io_cap, in_words + (size_t)B * c->Wp, sizeof(uint32_t)))) return rc;
+  for (int k = 0; k < arity; ++k)
+    GW_CUDA(c, cudaMemcpy2DAsync(c->io + (size_t)k * B * c->Wp, c->Wp * sizeof(uint32_t), ops[k],
+                                 W * sizeof(uint32_t), W * sizeof(uint32_t), B, cudaMemcpyHostToDevice, c->stream));
+  uint32_t* dout = c->io + in_words;
+  if ((rc = eval_stacked(c, opcode, c->io, arity, B, dout, c->Wp))) return rc;
+  GW_CUDA(c, cudaMemcpy2DAsync(out, W * sizeof(uint32_t), dout, c->Wp * sizeof(uint32_t), W * sizeof(uint32_t), B,
+                               cudaMemcpyDeviceToHost, c->stream));
+  GW_CUDA(c, cudaStreamSynchronize(c->stream));
+  return GW_OK;
+}
+
+int gw_wires_alloc(gw_ctx* c, int64_t slots) {
+  if (!c || slots < 0) return GW_ERR_ARG;
+  if (!c->have_params) return fail(c, GW_ERR_STATE, "parameters not set");
+  cudaSetDevice(c->device);
+  GW_CUDA(c, cudaStreamSynchronize(c->stream));
+  cudaFree(c->wires);
+  c->wires = nullptr;
+  c->wire_slots = 0;
+  if (slots == 0) return GW_OK;
+  GW_CUDA(c, cudaMalloc(&c->wires, (size_t)slots * c->Wp * sizeof(uint32_t)));
+  GW_CUDA(c, cudaMemsetAsync(c->wires, 0, (size_t)slots * c->Wp * sizeof(uint32_t), c->stream));
+  c->wire_slots = slots;
+  return GW_OK;
+}
+
+int gw_wires_device_ptr(gw_ctx* c, void** ptr, int64_t* stride) {
+  if (!c || !ptr || !stride) return GW_ERR_ARG;
+  *ptr = c->wires;
+  *stride = c->Wp;
+  return GW_OK;
+}
+
+static int check_ids(gw_ctx* c, const int64_t* ids, int64_t count) {
+  for (int64_t k = 0; k < count; ++k)
+    if (ids[k] < 0 || ids[k] >= c->wire_slots) return fail(c, GW_ERR_WIRE, "wire id out of range: " + std::to_string(ids[k]));
+  return GW_OK;
+}
+
+int gw_wires_put(gw_ctx* c, const int64_t* ids, const uint32_t* rows, int64_t count) {
+  if (!c || count < 0 || (count > 0 && (!ids || !rows))) return GW_ERR_ARG;
+  if (!c->wires) return fail(c, GW_ERR_STATE, "wire store not allocated");
+  int rc = check_ids(c, ids, count);
+  if (rc) return rc;
+  if (count == 0) return GW_OK;
+  cudaSetDevice(c->device);
+  const int W = c->p.n + 1;
+  // stage contiguous rows, then scatter with a copy per contiguous id run
+  int64_t k = 0;
+  while (k < count) {
+    int64_t run = 1;
+    while (k + run < count && ids[k + run] == ids[k] + run) ++run;
+    GW_CUDA(c, cudaMemcpy2DAsync(c->wires + (size_t)ids[k] * c->Wp, c->Wp * sizeof(uint32_t), rows + (size_t)k * W,
+                                 W * sizeof(uint32_t), W * sizeof(uint32_t), run, cudaMemcpyHostToDevice, c->stream));
+    k += run;
+  }
+  GW_CUDA(c, cudaStreamSynchronize(c->stream));
+  return GW_OK;
+}
+
+int gw_wires_get(gw_ctx* c, const int64_t* ids, uint32_t* rows, int64_t count) {
+  if (!c || count < 0 || (count > 0 && (!ids || !rows))) return GW_ERR_ARG;
+  if (!c->wires) return fail(c, GW_ERR_STATE, "wire store not allocated");
+  int rc = check_ids(c, ids, count);
+  if (rc) return rc;
+  if (count == 0) return GW_OK;
+  cudaSetDevice(c->device);
+  const int W = c->p.n + 1;
+  int64_t k = 0;
+  while (k < count) {
+    int64_t run = 1;
+    while (k + run < count && ids[k + run] == ids[k] + run) ++run;
+    GW_CUDA(c, cudaMemcpy2DAsync(rows + (size_t)k * W, W * sizeof(uint32_t), c->wires + (size_t)ids[k] * c->Wp,
+                                 c->Wp * sizeof(uint32_t), W * sizeof(uint32_t), run, cudaMemcpyDeviceToHost, c->stream));
+    k += run;
+  }
+  GW_CUDA(c, cudaStreamSynchronize(c->stream));
+  return GW_OK;
+}
+
+int gw_plan_create(gw_ctx* c, int64_t n_levels, const int64_t* offs, const int32_t* opcodes, const int32_t* operands,
+                   const int32_t* out_ids, gw_plan** out) {
+  if (!c || !out || n_levels < 0 || (n_levels > 0 && (!offs || !opcodes || !operands || !out_ids))) return GW_ERR_ARG;
+  if (!c->have_params) return fail(c, GW_ERR_STATE, "parameters not set");
+  *out = nullptr;
+  cudaSetDevice(c->device);
+  gw_plan* p = new gw_plan();
+  p->n_levels = n_levels;
+  std::vector<LinJob> jobs;
+  std::vector<KsUnit> units;
+  std::vector<CheapUnit> cheap;
+  for (int64_t lv = 0; lv < n_levels; ++lv) {
+    const size_t j0 = jobs.size(), u0 = units.size(), c0 = cheap.size();
+    p->job_off.push_back(j0);
+    p->unit_off.push_back(u0);
+    p->cheap_off.push_back(c0);
+    for (int64_t g = offs[lv]; g < offs[lv + 1]; ++g) {
+      const int op = opcodes[g];
+      const int ar = arity_of(op);
+      if (ar < 0) {
+        delete p;
+        return fail(c, GW_ERR_ARG, "unknown opcode in plan");
+      }
+      int32_t s[3] = {operands[3 * g], operands[3 * g + 1], operands[3 * g + 2]};
+      for (int k = 0; k < ar; ++k)
+        if (s[k] < 0 || s[k] >= c->wire_slots) {
+          delete p;
+          return fail(c, GW_ERR_WIRE, "operand wire out of range: " + std::to_string(s[k]));
+        }
+      if (out_ids[g] < 0 || out_ids[g] >= c->wire_slots) {
+        delete p;
+        return fail(c, GW_ERR_WIRE, "output wire out of range: " + std::to_string(out_ids[g]));
+      }
+      describe_gate(op, s[0], s[1], s[2], out_ids[g], c->p.mu, jobs, units, cheap);
+    }
+    // job indices inside units are level-local
+    for (size_t u = u0; u < units.size(); ++u) {
+      units[u].job0 -= (int32_t)j0;
+      if (units[u].job1 >= 0) units[u].job1 -= (int32_t)j0;
+    }
+    p->J.push_back((int)(jobs.size() - j0));
+    p->U.push_back((int)(units.size() - u0));
+    p->C.push_back((int)(cheap.size() - c0));
+    if (p->J.back() > p->max_jobs) p->max_jobs = p->J.back();
+  }
+  cudaError_t e = cudaSuccess;
+  if (!jobs.empty()) e = cudaMalloc(&p->jobs, jobs.size() * sizeof(LinJob));
+  if (e == cudaSuccess && !units.empty()) e = cudaMalloc(&p->units, units.size() * sizeof(KsUnit));
+  if (e == cudaSuccess && !cheap.empty()) e = cudaMalloc(&p->cheap, cheap.size() * sizeof(CheapUnit));
+  if (e == cudaSuccess && !jobs.empty())
+    e = cudaMemcpy(p->jobs, jobs.data(), jobs.size() * sizeof(LinJob), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !units.empty())
+    e = cudaMemcpy(p->units, units.data(), units.size() * sizeof(KsUnit), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !cheap.empty())
+    e = cudaMemcpy(p->cheap, cheap.data(), cheap.size() * sizeof(CheapUnit), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    gw_plan_destroy(c, p);
+    return fail(c, GW_ERR_CUDA, cudaGetErrorString(e));
+  }
+  *out = p;
+  return GW_OK;
+}
+
+int gw_plan_run_levels(gw_ctx* c, gw_plan* p, int64_t first, int64_t last) {
+  int rc = ready(c);
+  if (rc) return rc;
+  if (!p) return fail(c, GW_ERR_ARG, "null plan");
+  if (!c->wires) return fail(c, GW_ERR_STATE, "wire store not allocated");
+  if (first < 0) first = 0;
+  if (last > p->n_levels) last = p->n_levels;
+  cudaSetDevice(c->device);
+  for (int64_t lv = first; lv < last; ++lv) {
+    rc = run_level(c, c->wires, c->Wp, c->wires, c->Wp, p->jobs + p->job_off[lv], p->J[lv],
+                   p->units + p->unit_off[lv], p->U[lv], p->cheap + p->cheap_off[lv], p->C[lv]);
+    if (rc) return rc;
+  }
+  return GW_OK;
+}
+
+int gw_plan_run(gw_ctx* c, gw_plan* p) { return gw_plan_run_levels(c, p, 0, p ? p->n_levels : 0); }
+
+int gw_plan_destroy(gw_ctx* c, gw_plan* p) {
+  if (!p) return GW_OK;
+  if (c) cudaSetDevice(c->device);
+  cudaFree(p->jobs);
+  cudaFree(p->units);
+  cudaFree(p->cheap);
+  delete p;
+  return GW_OK;
+}
+
+int gw_timer_start(gw_ctx* c) {
+  if (!c) return GW_ERR_ARG;
+  GW_CUDA(c, cudaEventRecord(c->ev0, c->stream));
+  return GW_OK;
+}
+
+int gw_timer_stop(gw_ctx* c, float* ms) {
+  if (!c || !ms) return GW_ERR_ARG;
+  GW_CUDA(c, cudaEventRecord(c->ev1, c->stream));
+  GW_CUDA(c, cudaEventSynchronize(c->ev1));
+  GW_CUDA(c, cudaEventElapsedTime(ms, c->ev0, c->ev1));
+  return GW_OK;
+}
+
+int gw_launch_count(gw_ctx* c, int64_t* count) {
+  if (!c || !count) return GW_ERR_ARG;
+  *count = c->launches;
+  return GW_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,381 @@
+"""ctypes binding of the C ABI (include/gatewave_b200.h) and device contexts.
+
+This is the only place Python touches the CUDA engine.  There is no CPU
+fallback: if the shared library or a GPU is missing, every hot-path call
+raises ``EngineUnavailable``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from collections import OrderedDict
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_NAME = "libgatewave_b200.so"
+LIB_PATH = os.path.join(_HERE, LIB_NAME)
+
+GW_OK = 0
+GW_ERR_PARAM = -1
+GW_ERR_DIM = -2
+GW_ERR_STATE = -3
+GW_ERR_CUDA = -4
+GW_ERR_ARG = -5
+GW_ERR_WIRE = -6
+
+# gatewave.cggi.GateKind order (cggi.py:142-153) + the bootstrap-only opcode
+OPCODES = {"AND": 0, "OR": 1, "NAND": 2, "NOR": 3, "XOR": 4, "XNOR": 5, "NOT": 6, "MUX": 7,
+           "CONST0": 8, "CONST1": 9, "COPY": 10, "BOOTSTRAP": 11}
+
+# Every symbol include/gatewave_b200.h declares.
+EXPORTS = ("gw_version", "gw_device_count", "gw_create", "gw_destroy", "gw_last_error",
+           "gw_set_stream", "gw_sync", "gw_set_params", "gw_upload_keys", "gw_bk_fft_size",
+           "gw_download_bk_fft", "gw_blind_rotate", "gw_keyswitch", "gw_eval_gate_batch",
+           "gw_eval_gate_batch_device", "gw_wires_alloc", "gw_wires_put", "gw_wires_get",
+           "gw_wires_device_ptr", "gw_plan_create", "gw_plan_run", "gw_plan_run_levels",
+           "gw_plan_destroy", "gw_timer_start", "gw_timer_stop", "gw_launch_count")
+
+
+class EngineUnavailable(RuntimeError):
+    """The CUDA engine (library or GPU) is not available; there is no fallback."""
+
+
+class GwParams(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("N", ctypes.c_int32), ("bg_bits", ctypes.c_int32),
+                ("l", ctypes.c_int32), ("ks_base_bits", ctypes.c_int32),
+                ("ks_levels", ctypes.c_int32), ("mu", ctypes.c_uint32)]
+
+
+_P = ctypes.c_void_p
+_U32P = ctypes.POINTER(ctypes.c_uint32)
+_I32P = ctypes.POINTER(ctypes.c_int32)
+_I64P = ctypes.POINTER(ctypes.c_int64)
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library(path: str | None = None):
+    """Load (once) and type the engine library."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        path = path or os.environ.get("GATEWAVE_B200_LIB", LIB_PATH)
+        if not os.path.exists(path):
+            raise EngineUnavailable(
+                f"{path} not built; run `python -m paper_2306_11006_b200.build` "
+                "(nvcc, sm_100a)")
+        L = ctypes.CDLL(path)
+        sig = {
+            "gw_version": ([], ctypes.c_int),
+            "gw_device_count": ([ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+            "gw_create": ([ctypes.c_int, ctypes.POINTER(_P)], ctypes.c_int),
+            "gw_destroy": ([_P], ctypes.c_int),
+            "gw_last_error": ([_P], ctypes.c_char_p),
+            "gw_set_stream": ([_P, _P], ctypes.c_int),
+            "gw_sync": ([_P], ctypes.c_int),
+            "gw_set_params": ([_P, ctypes.POINTER(GwParams)], ctypes.c_int),
+            "gw_upload_keys": ([_P, _U32P, _U32P], ctypes.c_int),
+            "gw_bk_fft_size": ([_P, _I64P], ctypes.c_int),
+            "gw_download_bk_fft": ([_P, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+            "gw_blind_rotate": ([_P, _U32P, ctypes.c_int64, _U32P, _U32P], ctypes.c_int),
+            "gw_keyswitch": ([_P, _U32P, ctypes.c_int64, _U32P], ctypes.c_int),
+            "gw_eval_gate_batch": ([_P, ctypes.c_int, ctypes.POINTER(_U32P), ctypes.c_int,
+                                    ctypes.c_int64, _U32P], ctypes.c_int),
+            "gw_eval_gate_batch_device": ([_P, ctypes.c_int, ctypes.POINTER(_P), ctypes.c_int64,
+                                           ctypes.c_int, ctypes.c_int64, _P, ctypes.c_int64],
+                                          ctypes.c_int),
+            "gw_wires_alloc": ([_P, ctypes.c_int64], ctypes.c_int),
+            "gw_wires_put": ([_P, _I64P, _U32P, ctypes.c_int64], ctypes.c_int),
+            "gw_wires_get": ([_P, _I64P, _U32P, ctypes.c_int64], ctypes.c_int),
+            "gw_wires_device_ptr": ([_P, ctypes.POINTER(_P), _I64P], ctypes.c_int),
+            "gw_plan_create": ([_P, ctypes.c_int64, _I64P, _I32P, _I32P, _I32P,
+                                ctypes.POINTER(_P)], ctypes.c_int),
+            "gw_plan_run": ([_P, _P], ctypes.c_int),
+            "gw_plan_run_levels": ([_P, _P, ctypes.c_int64, ctypes.c_int64], ctypes.c_int),
+            "gw_plan_destroy": ([_P, _P], ctypes.c_int),
+            "gw_timer_start": ([_P], ctypes.c_int),
+            "gw_timer_stop": ([_P, ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
+            "gw_launch_count": ([_P, _I64P], ctypes.c_int),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+        return L
+
+
+def device_count() -> int:
+    n = ctypes.c_int(0)
+    load_library().gw_device_count(ctypes.byref(n))
+    return n.value
+
+
+def _u32(a):
+    return a.ctypes.data_as(_U32P)
+
+
+def _c_rows(a, width=None):
+    a = np.ascontiguousarray(a, dtype=np.uint32)
+    if width is not None and (a.ndim != 2 or a.shape[1] != width):
+        raise ValueError(f"expected rows of width {width}, got {a.shape}")
+    return a
+
+
+class Engine:
+    """One device context holding parameters and (optionally) keys."""
+
+    def __init__(self, n, N, bg_bits, l, ks_base_bits, ks_levels, mu, device: int | None = None):
+        self._lib = load_library()
+        if device is None:
+            device = default_device()
+        self.device = device
+        self.n, self.N, self.bg_bits, self.l = n, N, bg_bits, l
+        self.ks_base_bits, self.ks_levels, self.mu = ks_base_bits, ks_levels, mu
+        ctx = _P()
+        rc = self._lib.gw_create(device, ctypes.byref(ctx))
+        if rc != GW_OK or not ctx.value:
+            raise EngineUnavailable(f"gw_create(device={device}) failed ({rc}): no usable B200")
+        self._ctx = ctx
+        p = GwParams(n, N, bg_bits, l, ks_base_bits, ks_levels, mu & 0xFFFFFFFF)
+        self._check(self._lib.gw_set_params(self._ctx, ctypes.byref(p)))
+
+    # -- plumbing -----------------------------------------------------------
+    def _check(self, rc):
+        if rc == GW_OK:
+            return
+        msg = self._lib.gw_last_error(self._ctx).decode(errors="replace") if self._ctx else ""
+        from . import cggi  # late import: error types live with the API
+        if rc == GW_ERR_PARAM:
+            raise cggi.ParameterError(msg)
+        if rc == GW_ERR_DIM:
+            raise cggi.DimensionError(msg)
+        if rc == GW_ERR_WIRE:
+            from .runtime import EvaluateError
+            raise EvaluateError(msg)
+        if rc == GW_ERR_ARG:
+            raise ValueError(msg)
+        raise RuntimeError(f"gatewave-b200 engine error {rc}: {msg}")
+
+    def close(self):
+        if getattr(self, "_ctx", None) and self._ctx.value:
+            self._lib.gw_destroy(self._ctx)
+            self._ctx = _P()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._ctx
+
+    def sync(self):
+        self._check(self._lib.gw_sync(self._ctx))
+
+    def set_stream(self, stream_ptr: int | None):
+        self._check(self._lib.gw_set_stream(self._ctx, _P(stream_ptr or 0)))
+
+    def launch_count(self) -> int:
+        v = ctypes.c_int64(0)
+        self._check(self._lib.gw_launch_count(self._ctx, ctypes.byref(v)))
+        return v.value
+
+    def timer_start(self):
+        self._check(self._lib.gw_timer_start(self._ctx))
+
+    def timer_stop(self) -> float:
+        ms = ctypes.c_float(0)
+        self._check(self._lib.gw_timer_stop(self._ctx, ctypes.byref(ms)))
+        return float(ms.value)
+
+    # -- keys ---------------------------------------------------------------
+    def upload_keys(self, bk_data=None, ksk_data=None):
+        bk = None if bk_data is None else np.ascontiguousarray(bk_data, dtype=np.uint32)
+        ksk = None if ksk_data is None else np.ascontiguousarray(ksk_data, dtype=np.uint32)
+        if bk is not None and bk.shape != (self.n, 2 * self.l, 2, self.N):
+            from .cggi import DimensionError
+            raise DimensionError(f"bootstrapping key must be (n, 2l, 2, N), got {bk.shape}")
+        if ksk is not None and ksk.shape != (self.N, self.ks_levels, (1 << self.ks_base_bits) - 1,
+                                             self.n + 1):
+            from .cggi import DimensionError
+            raise DimensionError(f"keyswitch key has shape {ksk.shape}")
+        self._check(self._lib.gw_upload_keys(self._ctx, _u32(bk) if bk is not None else None,
+                                             _u32(ksk) if ksk is not None else None))
+
+    def bk_fft(self) -> np.ndarray:
+        """Device FFT-domain key as complex128, native layout [i][c][s][r][h][lane]."""
+        cnt = ctypes.c_int64(0)
+        self._check(self._lib.gw_bk_fft_size(self._ctx, ctypes.byref(cnt)))
+        out = np.empty(cnt.value, np.complex128)
+        self._check(self._lib.gw_download_bk_fft(
+            self._ctx, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return out
+
+    # -- seam 1 twins -------------------------------------------------------
+    def blind_rotate(self, lin, tv) -> np.ndarray:
+        lin = _c_rows(lin, self.n + 1)
+        tv = np.ascontiguousarray(tv, dtype=np.uint32)
+        if tv.shape != (2, self.N):
+            from .cggi import DimensionError
+            raise DimensionError(f"test vector must be (2, {self.N}), got {tv.shape}")
+        B = lin.shape[0]
+        acc = np.empty((B, 2, self.N), np.uint32)
+        if B:
+            self._check(self._lib.gw_blind_rotate(self._ctx, _u32(lin), B, _u32(tv), _u32(acc)))
+        return acc
+
+    def keyswitch(self, ext) -> np.ndarray:
+        ext = _c_rows(ext, self.N + 1)
+        B = ext.shape[0]
+        out = np.empty((B, self.n + 1), np.uint32)
+        if B:
+            self._check(self._lib.gw_keyswitch(self._ctx, _u32(ext), B, _u32(out)))
+        return out
+
+    # -- seam 2 -------------------------------------------------------------
+    def eval_gate_batch(self, opcode: int, mats, count: int) -> np.ndarray:
+        mats = [_c_rows(m, self.n + 1) for m in mats]
+        out = np.empty((count, self.n + 1), np.uint32)
+        if count == 0:
+            return out
+        arr = (_U32P * max(1, len(mats)))(*[_u32(m) for m in mats])
+        self._check(self._lib.gw_eval_gate_batch(self._ctx, opcode, arr, len(mats), count,
+                                                 _u32(out)))
+        return out
+
+    def eval_gate_batch_device(self, opcode: int, d_ops, in_stride: int, count: int, d_out: int,
+                               out_stride: int):
+        """Device pointers in/out (e.g. torch tensors' data_ptr()); enqueue only."""
+        arr = (_P * max(1, len(d_ops)))(*[_P(p) for p in d_ops])
+        self._check(self._lib.gw_eval_gate_batch_device(self._ctx, opcode, arr, in_stride,
+                                                        len(d_ops), count, _P(d_out),
+                                                        out_stride))
+
+    # -- seam 3: wire store + plans ------------------------------------------
+    def wires_alloc(self, slots: int):
+        self._check(self._lib.gw_wires_alloc(self._ctx, slots))
+
+    def wires_put(self, ids, rows):
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        rows = _c_rows(rows, self.n + 1)
+        if rows.shape[0] != ids.shape[0]:
+            raise ValueError("row count does not match id count")
+        self._check(self._lib.gw_wires_put(self._ctx, ids.ctypes.data_as(_I64P), _u32(rows),
+                                           ids.shape[0]))
+
+    def wires_get(self, ids) -> np.ndarray:
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        out = np.empty((ids.shape[0], self.n + 1), np.uint32)
+        self._check(self._lib.gw_wires_get(self._ctx, ids.ctypes.data_as(_I64P), _u32(out),
+                                           ids.shape[0]))
+        return out
+
+    def wires_device_ptr(self):
+        p = _P()
+        stride = ctypes.c_int64(0)
+        self._check(self._lib.gw_wires_device_ptr(self._ctx, ctypes.byref(p), ctypes.byref(stride)))
+        return p.value or 0, stride.value
+
+    def plan_create(self, level_offsets, opcodes, operands, out_ids) -> "Plan":
+        offs = np.ascontiguousarray(level_offsets, dtype=np.int64)
+        ops = np.ascontiguousarray(opcodes, dtype=np.int32)
+        opnd = np.ascontiguousarray(operands, dtype=np.int32).reshape(-1, 3)
+        outs = np.ascontiguousarray(out_ids, dtype=np.int32)
+        h = _P()
+        self._check(self._lib.gw_plan_create(
+            self._ctx, offs.shape[0] - 1, offs.ctypes.data_as(_I64P), ops.ctypes.data_as(_I32P),
+            opnd.ctypes.data_as(_I32P), outs.ctypes.data_as(_I32P), ctypes.byref(h)))
+        return Plan(self, h, offs.shape[0] - 1)
+
+
+class Plan:
+    def __init__(self, engine: Engine, handle, n_levels: int):
+        self.engine = engine
+        self._h = handle
+        self.n_levels = n_levels
+
+    def run(self, first: int = 0, last: int | None = None):
+        last = self.n_levels if last is None else last
+        e = self.engine
+        e._check(e._lib.gw_plan_run_levels(e._ctx, self._h, first, last))
+
+    def close(self):
+        if self._h and self._h.value:
+            self.engine._lib.gw_plan_destroy(self.engine._ctx, self._h)
+            self._h = _P()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------------
+# Device selection and the per-key context cache.
+# ---------------------------------------------------------------------------
+
+_device_override: int | None = None
+
+
+def set_device(device: int):
+    """Pin the CUDA ordinal new contexts are created on."""
+    global _device_override
+    _device_override = int(device)
+
+
+def default_device() -> int:
+    if _device_override is not None:
+        return _device_override
+    for var in ("GATEWAVE_DEVICE", "LOCAL_RANK"):
+        if var in os.environ:
+            return int(os.environ[var])
+    return 0
+
+
+_CACHE: "OrderedDict[tuple, tuple]" = OrderedDict()
+_CACHE_MAX = 3
+_cache_lock = threading.Lock()
+
+
+def params_tuple(params):
+    return (int(params.n), int(params.N), int(params.Bg_bits), int(params.l),
+            int(params.ks_base_bits), int(params.ks_levels), int(params.mu))
+
+
+def engine_for(params, bk_data=None, ksk_data=None, device: int | None = None) -> Engine:
+    """Context with these keys resident, uploaded once and cached.
+
+    The cache key is the identity + data pointer of the key arrays (the
+    reference passes ek.bk.ntt / ek.ksk.data on every call); a
+    strong reference keeps them alive so ids cannot be recycled.
+    """
+    dev = default_device() if device is None else device
+    key = (params_tuple(params), dev,
+           None if bk_data is None else (id(bk_data), bk_data.ctypes.data, bk_data.shape),
+           None if ksk_data is None else (id(ksk_data), ksk_data.ctypes.data, ksk_data.shape))
+    with _cache_lock:
+        hit = _CACHE.get(key)
+        if hit is not None:
+            _CACHE.move_to_end(key)
+            return hit[0]
+        eng = Engine(*params_tuple(params), device=dev)
+        eng.upload_keys(bk_data, ksk_data)
+        _CACHE[key] = (eng, bk_data, ksk_data)
+        while len(_CACHE) > _CACHE_MAX:
+            _, (old, _, _) = _CACHE.popitem(last=False)
+            old.close()
+        return eng
+
+
+def clear_cache():
+    with _cache_lock:
+        for eng, _, _ in _CACHE.values():
+            eng.close()
+        _CACHE.clear()
