@@ -116,6 +116,12 @@ int gw_plan_destroy(gw_ctx* ctx, gw_plan* plan);
 /* CUDA-event timer on the context stream (milliseconds between start/stop). */
 int gw_timer_start(gw_ctx* ctx);
 int gw_timer_stop(gw_ctx* ctx, float* ms);
+/* Optional per-stage CUDA-event accounting (roofline evidence): when on,
+ * every blind-rotation / keyswitch / other launch is bracketed by events.
+ * gw_stage_times syncs and returns summed milliseconds and processed items
+ * (bootstraps, output samples, 0) per stage: [blind_rotate, keyswitch, other]. */
+int gw_set_profiling(gw_ctx* ctx, int on);
+int gw_stage_times(gw_ctx* ctx, double* ms, int64_t* items, int reset);
 /* Number of engine kernel launches issued by this context so far. */
 int gw_launch_count(gw_ctx* ctx, int64_t* count);
 

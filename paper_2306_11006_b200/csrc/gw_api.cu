@@ -65,6 +65,10 @@ struct gw_ctx {
   std::map<uint64_t, BatchDesc> batch_desc;
   // timing / accounting
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool profile = false;                       // per-stage event pairs (gw_set_profiling)
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev[3];  // 0 blind rotate, 1 keyswitch, 2 other
+  std::vector<cudaEvent_t> ev_pool;
+  int64_t prof_items[3] = {0, 0, 0};
   int64_t launches = 0;
   std::string err;
 };
@@ -301,6 +305,30 @@ int launch_cheap(gw_ctx* c, const uint32_t* src, int64_t src_stride, const Cheap
   return GW_OK;
 }
 
+cudaEvent_t pooled_event(gw_ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Stage bracket: records an event pair around `body` when profiling is on.
+template <typename F>
+int staged(gw_ctx* c, int stage, int64_t items, F&& body) {
+  if (!c->profile) return body();
+  cudaEvent_t a = pooled_event(c), b = pooled_event(c);
+  cudaEventRecord(a, c->stream);
+  int rc = body();
+  cudaEventRecord(b, c->stream);
+  c->prof_ev[stage].emplace_back(a, b);
+  c->prof_items[stage] += items;
+  return rc;
+}
+
 int ready(gw_ctx* c, bool need_bk = true, bool need_ksk = true) {
   if (!c) return GW_ERR_ARG;
   if (!c->have_params) return fail(c, GW_ERR_STATE, "parameters not set");
@@ -316,7 +344,7 @@ int run_level(gw_ctx* c, const uint32_t* src, int64_t src_stride, uint32_t* dst,
   if (J > 0) {
     if ((rc = ensure(c, &c->lin, &c->lin_cap, (size_t)J * c->Wp, sizeof(uint32_t)))) return rc;
     if ((rc = ensure(c, &c->acc, &c->acc_cap, (size_t)J * 2 * c->p.N, sizeof(uint32_t)))) return rc;
-    if ((rc = launch_lin(c, src, src_stride, jobs, J))) return rc;
+    if ((rc = staged(c, 2, 0, [&] { return launch_lin(c, src, src_stride, jobs, J); }))) return rc;
     BrArgs a;
     a.lin = c->lin;
     a.lin_stride = c->Wp;
@@ -331,10 +359,11 @@ int run_level(gw_ctx* c, const uint32_t* src, int64_t src_stride, uint32_t* dst,
     for (int j = 1; j <= c->p.l; ++j) off += (uint64_t)(1u << (c->p.bg_bits - 1)) << (32 - j * c->p.bg_bits);
     a.offs = (uint32_t)(off & 0xFFFFFFFFull);
     a.gates_per_cta = 1;
-    if ((rc = launch_br(c, a))) return rc;
-    if ((rc = launch_ks(c, c->acc, units, U, dst, dst_stride))) return rc;
+    if ((rc = staged(c, 0, J, [&] { return launch_br(c, a); }))) return rc;
+    if ((rc = staged(c, 1, U, [&] { return launch_ks(c, c->acc, units, U, dst, dst_stride); }))) return rc;
   }
-  if ((rc = launch_cheap(c, src, src_stride, cheap, C, dst, dst_stride))) return rc;
+  if ((rc = staged(c, 2, 0, [&] { return launch_cheap(c, src, src_stride, cheap, C, dst, dst_stride); })))
+    return rc;
   return GW_OK;
 }
 
@@ -460,6 +489,12 @@ int gw_destroy(gw_ctx* c) {
   cudaFree(c->wires);
   for (auto& kv : c->batch_desc) cudaFree(kv.second.mem);
   if (c->desc_host) cudaFreeHost(c->desc_host);
+  for (auto& v : c->prof_ev)
+    for (auto& pr : v) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -949,6 +984,36 @@ int gw_timer_stop(gw_ctx* c, float* ms) {
   GW_CUDA(c, cudaEventRecord(c->ev1, c->stream));
   GW_CUDA(c, cudaEventSynchronize(c->ev1));
   GW_CUDA(c, cudaEventElapsedTime(ms, c->ev0, c->ev1));
+  return GW_OK;
+}
+
+int gw_set_profiling(gw_ctx* c, int on) {
+  if (!c) return GW_ERR_ARG;
+  c->profile = on != 0;
+  return GW_OK;
+}
+
+int gw_stage_times(gw_ctx* c, double* ms /* [3] */, int64_t* items /* [3] */, int reset) {
+  if (!c || !ms) return GW_ERR_ARG;
+  GW_CUDA(c, cudaStreamSynchronize(c->stream));
+  for (int k = 0; k < 3; ++k) {
+    double tot = 0;
+    for (auto& pr : c->prof_ev[k]) {
+      float t = 0;
+      GW_CUDA(c, cudaEventElapsedTime(&t, pr.first, pr.second));
+      tot += t;
+    }
+    ms[k] = tot;
+    if (items) items[k] = c->prof_items[k];
+    if (reset) {
+      for (auto& pr : c->prof_ev[k]) {
+        c->ev_pool.push_back(pr.first);
+        c->ev_pool.push_back(pr.second);
+      }
+      c->prof_ev[k].clear();
+      c->prof_items[k] = 0;
+    }
+  }
   return GW_OK;
 }
 

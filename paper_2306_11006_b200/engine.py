@@ -35,7 +35,8 @@ EXPORTS = ("gw_version", "gw_device_count", "gw_create", "gw_destroy", "gw_last_
            "gw_download_bk_fft", "gw_blind_rotate", "gw_keyswitch", "gw_eval_gate_batch",
            "gw_eval_gate_batch_device", "gw_wires_alloc", "gw_wires_put", "gw_wires_get",
            "gw_wires_device_ptr", "gw_plan_create", "gw_plan_run", "gw_plan_run_levels",
-           "gw_plan_destroy", "gw_timer_start", "gw_timer_stop", "gw_launch_count")
+           "gw_plan_destroy", "gw_timer_start", "gw_timer_stop", "gw_set_profiling",
+           "gw_stage_times", "gw_launch_count")
 
 
 class EngineUnavailable(RuntimeError):
@@ -98,6 +99,9 @@ def load_library(path: str | None = None):
             "gw_plan_destroy": ([_P, _P], ctypes.c_int),
             "gw_timer_start": ([_P], ctypes.c_int),
             "gw_timer_stop": ([_P, ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
+            "gw_set_profiling": ([_P, ctypes.c_int], ctypes.c_int),
+            "gw_stage_times": ([_P, ctypes.POINTER(ctypes.c_double), _I64P, ctypes.c_int],
+                               ctypes.c_int),
             "gw_launch_count": ([_P, _I64P], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
@@ -185,6 +189,17 @@ class Engine:
         v = ctypes.c_int64(0)
         self._check(self._lib.gw_launch_count(self._ctx, ctypes.byref(v)))
         return v.value
+
+    def set_profiling(self, on: bool = True):
+        self._check(self._lib.gw_set_profiling(self._ctx, 1 if on else 0))
+
+    def stage_times(self, reset: bool = True):
+        """{stage: (ms, items)} for blind_rotate / keyswitch / other since last reset."""
+        ms = (ctypes.c_double * 3)()
+        items = (ctypes.c_int64 * 3)()
+        self._check(self._lib.gw_stage_times(self._ctx, ms, items, 1 if reset else 0))
+        names = ("blind_rotate", "keyswitch", "other")
+        return {names[k]: (float(ms[k]), int(items[k])) for k in range(3)}
 
     def timer_start(self):
         self._check(self._lib.gw_timer_start(self._ctx))

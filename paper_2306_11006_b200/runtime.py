@@ -1,0 +1,236 @@
+"""Level-by-level netlist evaluation on the device-resident wire store.
+
+Drop-in for gatewave/runtime.py (reference): `evaluate(c, schedule, inputs,
+keys) -> (outputs, Metrics)` with the same validation, exceptions, metrics
+and bit-identical outputs for every worker count.  What changed:
+
+* the reference's host WireStore + thread pool + per-wave fences
+  (runtime.py:76-222) become ONE device-resident wire store in HBM and a
+  precompiled level plan: per level a single fused launch set (all opcodes of
+  the level together) on one CUDA stream, so ordering replaces fences and no
+  host synchronisation happens between levels;
+* the SSA guards the reference checks on every read/write (runtime.py:83-96)
+  are checked once, statically, over the whole plan before anything runs;
+* with several GPUs (torch.distributed, one process per GPU) each rank runs
+  the schedule slices whose `worker` equals its rank and, after every level,
+  exchanges only the produced wires that another rank reads later
+  (exchange.py).
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import Mapping
+
+import numpy as np
+
+from .cggi import (BOOTSTRAPS_PER_GATE, GATE_ARITY, DimensionError, EvalKey, _as_eval_key,
+                   as_kind)
+from .circuit import Circuit
+from .scheduler import Schedule
+
+
+class EvaluateError(RuntimeError):
+    """Inputs do not match the circuit, or an internal invariant broke."""
+
+
+@dataclass
+class Metrics:
+    """Same fields and JSON shape as the reference's Metrics (runtime.py:42-73).
+
+    Times come from CUDA events on the engine stream (device time per wave);
+    spans are (wave, worker, start, end) on the monotonic clock."""
+
+    total_gates: int = 0
+    workers: int = 0
+    bootstrap_count: int = 0
+    ntt_forward_count: int = 0
+    ntt_inverse_count: int = 0
+    wall_time_seconds: float = 0.0
+    gates_per_second: float = 0.0
+    per_wave_wall_time: list[float] = field(default_factory=list)
+    per_worker_busy_time: list[float] = field(default_factory=list)
+    spans: list[tuple[int, int, float, float]] = field(default_factory=list)
+    device_time_seconds: float = 0.0
+    gpus: int = 1
+
+    def as_dict(self) -> dict:
+        return {
+            "total_gates": self.total_gates,
+            "workers": self.workers,
+            "bootstrap_count": self.bootstrap_count,
+            "ntt_forward_count": self.ntt_forward_count,
+            "ntt_inverse_count": self.ntt_inverse_count,
+            "wall_time_seconds": self.wall_time_seconds,
+            "gates_per_second": self.gates_per_second,
+            "per_wave_wall_time": self.per_wave_wall_time,
+            "per_worker_busy_time": self.per_worker_busy_time,
+        }
+
+
+class WireStore:
+    """Host mirror of the reference's SSA-guarded wire store (runtime.py:76-96).
+    Used for host-side plans and tests; the engine keeps ciphertexts in HBM."""
+
+    def __init__(self, slots: int, width: int):
+        self._rows = np.zeros((slots, width), dtype=np.uint32)
+        self._written = np.zeros(slots, dtype=bool)
+
+    def write_rows(self, wire_ids, rows: np.ndarray) -> None:
+        idx = np.asarray(wire_ids, dtype=np.int64)
+        if np.any(self._written[idx]):
+            raise EvaluateError(f"wire {int(idx[self._written[idx]][0])} written twice")
+        self._rows[idx] = rows
+        self._written[idx] = True
+
+    def read_rows(self, wire_ids) -> np.ndarray:
+        idx = np.asarray(wire_ids, dtype=np.int64)
+        if not np.all(self._written[idx]):
+            raise EvaluateError(f"wire {int(idx[~self._written[idx]][0])} read before it was written")
+        return self._rows[idx]
+
+
+def check_inputs(c: Circuit, inputs: Mapping[str, np.ndarray], n: int) -> dict[str, np.ndarray]:
+    """runtime.py:99-119: same checks, same exception types and messages."""
+    names = {p.name for p in c.inputs}
+    for name in inputs:
+        if name not in names:
+            raise EvaluateError(f"unknown input group {name!r}")
+    mats = {}
+    for p in c.inputs:
+        if p.name not in inputs:
+            raise EvaluateError(f"missing input group {p.name!r}")
+        m = np.ascontiguousarray(inputs[p.name], dtype=np.uint32)
+        if m.ndim != 2 or m.shape[0] != p.width:
+            raise EvaluateError(f"input {p.name!r} must provide {p.width} rows, got shape {m.shape}")
+        if m.shape[1] != n + 1:
+            raise DimensionError(f"input {p.name!r} samples have dimension {m.shape[1] - 1}, "
+                                 f"parameters expect {n}")
+        mats[p.name] = m
+    return mats
+
+
+_OPC = {"AND": 0, "OR": 1, "NAND": 2, "NOR": 3, "XOR": 4, "XNOR": 5, "NOT": 6, "MUX": 7,
+        "CONST0": 8, "CONST1": 9, "COPY": 10}
+
+
+@dataclass
+class LevelPlan:
+    """Flat per-level gate arrays for one worker (GPU), checked for SSA order."""
+
+    level_offsets: np.ndarray   # (levels + 1,) int64
+    opcodes: np.ndarray         # (gates,) int32
+    operands: np.ndarray        # (gates, 3) int32, -1 padded
+    out_ids: np.ndarray         # (gates,) int32
+    bootstraps: int
+    gates: int
+
+
+def compile_plan(c: Circuit, schedule: Schedule, worker: int | None = None) -> LevelPlan:
+    """Flatten a schedule into level arrays.  worker=None merges every worker's
+    batches into one level (single GPU); worker=k keeps rank k's slices only.
+
+    Static SSA check over the whole schedule (the reference's per-access
+    WireStore guards, runtime.py:83-96): every wire is written once, and read
+    only in a wave strictly after the one that writes it.
+    """
+    by_id = {g.id: g for g in c.gates}
+    scheduled = [gid for wave in schedule.waves for b in wave for gid in b.gate_ids]
+    if sorted(scheduled) != sorted(by_id):
+        raise EvaluateError("schedule does not cover this circuit's gates")
+    written_at: dict[int, int] = {w: -1 for w in c.input_wires}
+    for wi, wave in enumerate(schedule.waves):
+        for b in wave:
+            for gid in b.gate_ids:
+                for w in by_id[gid].operands:
+                    if written_at.get(w, wi) >= wi:
+                        raise EvaluateError(f"wire {w} read before it was written")
+        for b in wave:
+            for gid in b.gate_ids:
+                if gid in written_at:
+                    raise EvaluateError(f"wire {gid} written twice")
+                written_at[gid] = wi
+    offs, codes, opnd, outs = [0], [], [], []
+    boots = 0
+    for wave in schedule.waves:
+        for b in wave:
+            if worker is not None and b.worker != worker:
+                continue
+            kind = as_kind(b.opcode)
+            ar = GATE_ARITY[kind]
+            boots += BOOTSTRAPS_PER_GATE[kind] * len(b.gate_ids)
+            for gid in b.gate_ids:
+                g = by_id[gid]
+                if as_kind(g.opcode) is not kind or len(g.operands) != ar:
+                    raise EvaluateError(f"gate {gid} does not match its batch opcode")
+                codes.append(_OPC[kind.value])
+                ops = list(g.operands) + [-1] * (3 - ar)
+                opnd.append(ops)
+                outs.append(gid)
+        offs.append(len(codes))
+    return LevelPlan(level_offsets=np.asarray(offs, np.int64),
+                     opcodes=np.asarray(codes, np.int32),
+                     operands=np.asarray(opnd, np.int32).reshape(-1, 3),
+                     out_ids=np.asarray(outs, np.int32), bootstraps=boots, gates=len(codes))
+
+
+def evaluate(c: Circuit, schedule: Schedule, inputs: Mapping[str, np.ndarray], keys,
+             *, group=None) -> tuple[dict[str, np.ndarray], Metrics]:
+    """Run every gate of c over encrypted inputs on the GPU(s).
+
+    Single process: all of the schedule's worker slices run on this process's
+    GPU (the worker split only matters across GPUs).  With a torch.distributed
+    process group (`group`, or the default group when initialised and larger
+    than one), rank k runs the slices of worker k and levels are joined by the
+    wire exchange; every rank returns the full outputs.
+    """
+    ek: EvalKey = _as_eval_key(keys)
+    p = ek.params
+    mats = check_inputs(c, inputs, p.n)
+    world, rank = _world(group)
+    if world > 1:
+        from .exchange import evaluate_distributed
+        return evaluate_distributed(c, schedule, mats, ek, group=group)
+
+    plan = compile_plan(c, schedule, worker=None)
+    eng = ek.engine()
+    eng.wires_alloc(c.max_wire + 1)
+    for port in c.inputs:
+        eng.wires_put(np.asarray(port.wires, np.int64), mats[port.name])
+    metrics = Metrics(total_gates=len(c.gates), workers=schedule.workers, gpus=1)
+    handle = eng.plan_create(plan.level_offsets, plan.opcodes, plan.operands, plan.out_ids)
+    try:
+        per_wave = []
+        t0 = time.monotonic()
+        for w in range(len(schedule.waves)):
+            s = time.monotonic()
+            eng.timer_start()
+            handle.run(w, w + 1)
+            ms = eng.timer_stop()
+            e = time.monotonic()
+            per_wave.append(ms / 1e3)
+            metrics.spans.append((w, 0, s, e))
+        t1 = time.monotonic()
+    finally:
+        handle.close()
+    metrics.bootstrap_count = plan.bootstraps
+    metrics.ntt_forward_count = 2 * p.l * p.n * plan.bootstraps
+    metrics.ntt_inverse_count = 2 * p.n * plan.bootstraps
+    metrics.wall_time_seconds = t1 - t0
+    metrics.device_time_seconds = float(sum(per_wave))
+    metrics.gates_per_second = (len(c.gates) / metrics.wall_time_seconds
+                                if metrics.wall_time_seconds > 0 else 0.0)
+    metrics.per_wave_wall_time = per_wave
+    metrics.per_worker_busy_time = [metrics.device_time_seconds] + [0.0] * (schedule.workers - 1)
+    outputs = {port.name: eng.wires_get(np.asarray(port.wires, np.int64)) for port in c.outputs}
+    return outputs, metrics
+
+
+def _world(group):
+    try:
+        import torch.distributed as dist
+    except Exception:  # pragma: no cover - torch is part of the image
+        return 1, 0
+    if group is None and not (dist.is_available() and dist.is_initialized()):
+        return 1, 0
+    return dist.get_world_size(group), dist.get_rank(group)
