@@ -205,7 +205,10 @@ def run_ours(args):
     ks, A, B, bits_a, bits_b = _workload(P, rank, args.gates)
     ek = ks.eval_key()
     eng = ek.engine()
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream: the engine and the timing events share it
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    assert stream.cuda_stream != 0
     eng.set_stream(stream.cuda_stream)
     G = args.gates
     W = P.n + 1
@@ -270,7 +273,7 @@ def run_ours(args):
                 "kernel": "k_blind_rotate<10,2>",
                 "per_launch_ms": br_ms / launches_br,
                 "work_per_launch": f"{G} bootstraps x {flops_per_bootstrap} FLOP",
-                "kernel_share_of_step": br_ms / sum(step_ms),
+                "kernel_share_of_step": br_ms / max(sum(step_ms), 1e-9),
                 "keyswitch_ms_per_launch": ks_ms / launches_br,
                 "bk_stream_gbs": bk_bytes / (br_ms / launches_br / 1e3) / 1e9,
                 "peak_source": "measured DFMA peak, tools/microbench/pipes.cu "

@@ -28,11 +28,12 @@ struct BrArgs {
   int gates_per_cta;
 };
 
-// Bootstrapping key, FFT domain: [i][c][s][r][h][lane] complex, scaled by 1/M.
+// Bootstrapping key, FFT domain: [i][c][h][s][r][lane] complex, scaled by 1/M.
+// One (i, c, h) slice is the contiguous slab one MAC warp consumes per step.
 template <int LOGN, int LEV>
 __host__ __device__ __forceinline__ size_t bk_index(int i, int c, int s, int r, int h, int l) {
   using G = Geo<LOGN>;
-  return ((((size_t)(i * 2 + c) * G::P + s) * (2 * LEV) + r) * 2 + h) * G::L + l;
+  return ((((size_t)(i * 2 + c) * 2 + h) * G::P + s) * (2 * LEV) + r) * G::L + l;
 }
 
 template <int LOGN, int LEV>
@@ -151,15 +152,16 @@ __global__ void __launch_bounds__(256, 1) k_blind_rotate(BrArgs a) {
     // ---- MAC against BK_i slab of component c (cggi.py:648-657) ----
     double2 o0[P], o1[P];
     {
-      const double2* bkc = a.bk + bk_index<LOGN, LEV>(i, c, 0, 0, 0, l);
+      const double2* bk0 = a.bk + bk_index<LOGN, LEV>(i, c, 0, 0, 0, l);
+      const double2* bk1 = a.bk + bk_index<LOGN, LEV>(i, c, 0, 0, 1, l);
 #pragma unroll
       for (int s = 0; s < P; ++s) {
         double2 s0 = make_double2(0.0, 0.0), s1 = make_double2(0.0, 0.0);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const double2 d = xb_g[(size_t)r * G::TILE + s * L + l];
-          const double2 b0 = __ldg(bkc + ((size_t)(s * R + r) * 2 + 0) * L);
-          const double2 b1 = __ldg(bkc + ((size_t)(s * R + r) * 2 + 1) * L);
+          const double2 b0 = __ldg(bk0 + (size_t)(s * R + r) * L);
+          const double2 b1 = __ldg(bk1 + (size_t)(s * R + r) * L);
           s0 = cfma(s0, d, b0);
           s1 = cfma(s1, d, b1);
         }

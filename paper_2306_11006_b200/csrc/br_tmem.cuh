@@ -1,0 +1,224 @@
+// br_tmem.cuh -- blind rotation v2: 4 warps per gate, bootstrapping key
+// double-buffered in Tensor Memory (reference: gatewave/cggi.py:592-667).
+//
+// CTA = GC gates x 4 warps.  Warp o (= its TMEM sub-partition) of a gate
+//   * forward: row r = o of the 2l gadget-digit rows (cggi.py:627-647):
+//     rotate-subtract + decompose acc[c_r] (smem), fold, FFT, D^_r -> smem;
+//   * MAC (cggi.py:648-657): output o = (c, h): sum_r D^_r * BK_i[c][h][r]
+//     with the key slab read from TMEM (tcgen05.ld), D^ from smem;
+//   * inverse + round + acc[c] += v << 16h (cggi.py:658-666, smem atomics:
+//     wrap-around adds commute, so the result is exact for any order).
+// The key slab of step i+1 (one 32 KB (c,h) slice per sub-partition, 128 KB
+// total) is streamed from L2 into the other TMEM buffer in four batches
+// issued at the phase boundaries of step i, so its latency hides behind the
+// FFTs; the GC warps of a sub-partition split the slice.
+#pragma once
+#include "blind_rotate.cuh"
+#include "tmem.cuh"
+
+namespace gw {
+
+template <int LOGN, int LEV>
+struct TmGeo {
+  using G = Geo<LOGN>;
+  static constexpr int R = 2 * LEV;
+  static constexpr int COLS = G::P * R * 4;  // one buffer: P slots x R rows x complex (4 cols)
+  static constexpr int ALLOC = (2 * COLS) <= 32 ? 32 : (2 * COLS) <= 64 ? 64 : (2 * COLS) <= 128 ? 128
+                               : (2 * COLS) <= 256 ? 256 : 512;
+  static_assert(2 * COLS <= 512, "two key slabs must fit the 512 TMEM columns");
+  static size_t smem_bytes(int gc, int n) {
+    const size_t lin_words = ((size_t)n + 1 + 3) & ~(size_t)3;
+    return 16 /*tmem slot*/ + sizeof(double2) * G::TILE /*tw1'*/ +
+           (size_t)gc * (sizeof(double2) * R * G::TILE + 2 * G::N * sizeof(uint32_t) +
+                         lin_words * sizeof(uint32_t));
+  }
+};
+
+template <int LOGN, int LEV, int GC>
+__global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
+  using G = Geo<LOGN>;
+  using T = TmGeo<LOGN, LEV>;
+  constexpr int N = G::N, M = G::M, P = G::P, L = G::L, R = T::R, COLS = T::COLS;
+  // fill items per warp per step: its share of one (c,h) slice
+  constexpr int ITEMS = P * R / GC;        // complex values per lane
+  constexpr int NB = 4;                    // batches per step
+  constexpr int BS = ITEMS / NB > 0 ? ITEMS / NB : 1;
+  static_assert(ITEMS % NB == 0 || ITEMS < NB, "fill batches must tile the slice");
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* tm_slot = reinterpret_cast<uint32_t*>(smem_raw);
+  double2* tw1 = reinterpret_cast<double2*>(smem_raw + 16);
+  double2* xbuf_all = tw1 + G::TILE;
+  uint32_t* acc_all = reinterpret_cast<uint32_t*>(xbuf_all + (size_t)GC * R * G::TILE);
+  const size_t lin_words = ((size_t)a.n + 1 + 3) & ~(size_t)3;
+  uint32_t* lin_all = acc_all + (size_t)GC * 2 * N;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, l = lane & (L - 1);
+  const int gl = warp >> 2, o = warp & 3;
+  const int co = o >> 1, ho = o & 1;
+  const int g = blockIdx.x * GC + gl;
+  const bool active = g < a.B;
+
+  for (int t = threadIdx.x; t < G::TILE; t += blockDim.x) tw1[t] = a.tables[2 * G::TILE + t];
+  if (warp == 0) tm_alloc(tm_slot, T::ALLOC);
+
+  uint32_t* lin_s = lin_all + (size_t)gl * lin_words;
+  uint32_t* acc_g = acc_all + (size_t)gl * 2 * N;
+  double2* xb = xbuf_all + (size_t)gl * R * G::TILE;  // [row][slot][lane]
+  if (active) {
+    const uint32_t* src = a.lin + (size_t)g * a.lin_stride;
+    for (int t = o * 32 + lane; t <= a.n; t += 128) lin_s[t] = src[t];
+  }
+  tm_fence_before();
+  __syncthreads();
+  tm_fence_after();
+  const uint32_t tm_base = *tm_slot;
+  const uint32_t tm_warp = tm_base + ((uint32_t)(32 * o) << 16);
+
+  const uint32_t two_n_mask = 2 * N - 1;
+  const uint32_t rshift = 32 - (LOGN + 1);
+  const uint32_t radd = 1u << (32 - (LOGN + 1) - 1);
+  const uint32_t base_mask = (1u << a.bg_bits) - 1;
+  const int32_t half_base = 1 << (a.bg_bits - 1);
+
+  // ---- key-slab streaming into TMEM ----------------------------------------
+  // item t of this warp: slot s = (t / R) * GC + gl, row r = t % R
+  auto item_src = [&](int i, int t) -> const double2* {
+    const int s = (t / R) * GC + gl, r = t % R;
+    return a.bk + bk_index<LOGN, LEV>(i, co, s, r, ho, l);
+  };
+  auto item_col = [&](int buf, int t) -> uint32_t {
+    const int s = (t / R) * GC + gl, r = t % R;
+    return (uint32_t)(buf * COLS + (s * R + r) * 4);
+  };
+  double2 fb[2][BS];  // up to two batches in flight
+  auto issue = [&](int slot, int i, int batch) {
+#pragma unroll
+    for (int k = 0; k < BS; ++k) {
+      const int t = batch * BS + k;
+      fb[slot][k] = t < ITEMS ? __ldg(item_src(i, t)) : make_double2(0.0, 0.0);
+    }
+  };
+  auto store = [&](int slot, int buf, int batch) {
+#pragma unroll
+    for (int k = 0; k < BS; ++k) {
+      const int t = batch * BS + k;
+      if (t < ITEMS) tm_st4(tm_warp + item_col(buf, t), fb[slot][k]);
+    }
+  };
+
+  // prologue: slab of step 0 into buffer 0 (all gates' warps, even inactive ones)
+  for (int b = 0; b < NB; ++b) {
+    issue(0, 0, b);
+    store(0, 0, b);
+  }
+  // acc <- tv * X^{-bbar} (cggi.py:612-622): warp o < 2 initialises component o
+  if (active && o < 2) {
+    const uint32_t bbar = ((lin_s[a.n] + radd) >> rshift) & two_n_mask;
+    const uint32_t k = (2 * N - bbar) & two_n_mask;
+    const uint32_t* tvc = a.tv + o * N;
+    for (int j = lane; j < N; j += 32) {
+      const uint32_t m = ((uint32_t)j - k) & two_n_mask;
+      acc_g[o * N + j] = m < (uint32_t)N ? tvc[m] : 0u - tvc[m - N];
+    }
+  }
+  tm_wait_st();
+  tm_fence_before();
+  __syncthreads();
+  tm_fence_after();
+
+  const int bar_id = 1 + gl;
+  const bool owner = lane < L;
+  for (int i = 0; i < a.n; ++i) {
+    const int cur = i & 1, nxt = cur ^ 1;
+    const bool pre = i + 1 < a.n;
+    if (pre) issue(0, i + 1, 0);  // S0
+    // ---- forward: row r = o, r < R ----
+    if (active && o < R) {
+      const int cr = o / LEV, lv = o % LEV;
+      const uint32_t* A = acc_g + cr * N;
+      const uint32_t abar = ((lin_s[i] + radd) >> rshift) & two_n_mask;
+      const int sh = 32 - (lv + 1) * a.bg_bits;
+      double2 x[P];
+#pragma unroll
+      for (int m1 = 0; m1 < P; ++m1) {
+        int32_t d[2];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const uint32_t j = (uint32_t)(L * m1 + l + hh * M);
+          const uint32_t idx = (j - abar) & two_n_mask;
+          const uint32_t v = A[idx & (N - 1)];
+          const uint32_t rot = (idx & N) ? 0u - v : v;
+          const uint32_t buf = rot - A[j] + a.offs;
+          d[hh] = (int32_t)((buf >> sh) & base_mask) - half_base;
+        }
+        // lane-independent part of the twist; the per-lane part lives in tw1'
+        x[m1] = cmul(make_double2(small_int_to_double(d[0]), small_int_to_double(d[1])),
+                     c_root64[G::CSTEP * m1]);
+      }
+      double2* tile = xb + (size_t)o * G::TILE;
+      fft_forward<LOGN, true>(x, tile, tw1, l);
+      __syncwarp();
+#pragma unroll
+      for (int s = 0; s < P; ++s) tile[s * L + l] = x[s];
+    }
+    if (pre) {  // S1
+      store(0, nxt, 0);
+      issue(0, i + 1, 1);
+    }
+    named_barrier(bar_id, 128);
+    // ---- MAC: output (co, ho) over all R rows, key from TMEM ----
+    double2 acc[P];
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      double2 kr[R];
+      if constexpr (R == 4) {
+        tm_ld16(tm_warp + (uint32_t)(cur * COLS + s * R * 4), kr);
+      } else if constexpr (R == 2) {
+        tm_ld8(tm_warp + (uint32_t)(cur * COLS + s * R * 4), kr);
+      }
+      double2 sum = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int r = 0; r < R; ++r) sum = cfma(sum, xb[(size_t)r * G::TILE + s * L + l], kr[r]);
+      acc[s] = sum;
+    }
+    named_barrier(bar_id, 128);
+    if (pre) {  // S2
+      store(0, nxt, 1);
+      issue(0, i + 1, 2);
+      issue(1, i + 1, 3);
+    }
+    // ---- inverse, untwist, round, accumulate ----
+    if (active) {
+      fft_inverse<LOGN, true>(acc, xb + (size_t)o * G::TILE, tw1, l);
+      uint32_t* Ac = acc_g + co * N;
+      const int shift = 16 * ho;
+#pragma unroll
+      for (int m1 = 0; m1 < P; ++m1) {
+        const double2 v = cmulc(acc[m1], c_root64[G::CSTEP * m1]);
+        const uint32_t j = (uint32_t)(L * m1 + l);
+        if (owner) {
+          atomicAdd(Ac + j, round_mod32(v.x) << shift);
+          atomicAdd(Ac + j + M, round_mod32(v.y) << shift);
+        }
+      }
+    }
+    if (pre) {  // S3
+      store(0, nxt, 2);
+      store(1, nxt, 3);
+    }
+    tm_wait_st();
+    tm_fence_before();
+    __syncthreads();
+    tm_fence_after();
+  }
+  if (active && o < 2) {
+    uint32_t* dst = a.acc_out + ((size_t)g * 2 + o) * N;
+    for (int j = lane; j < N; j += 32) dst[j] = acc_g[o * N + j];
+  }
+  tm_fence_before();
+  __syncthreads();
+  if (warp == 0) tm_dealloc(tm_base, T::ALLOC);
+}
+
+}  // namespace gw

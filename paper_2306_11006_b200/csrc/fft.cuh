@@ -31,6 +31,8 @@ struct Geo {
   static_assert(L <= 32, "one warp per transform");
   // smem elements (double2) of one P x L tile
   static constexpr int TILE = P * L;
+  // e^{i pi L m1 / N} = c_root64[CSTEP * m1]: lane-independent part of the twist
+  static constexpr int CSTEP = 32 * L / N;
 };
 
 template <int LOGP>
@@ -105,14 +107,16 @@ __device__ __forceinline__ int swz(int k1, int col) { return col ^ ((k1 & 3) << 
 // Out: x[s] = Z[k(l, s)], k = k1 + P*(c + P*d), k1 = l>>1, b = l&1,
 //      c = b*P/2 + s%(P/2), d = s/(P/2).
 // tw1: smem [k1][l] = e^{2 pi i l k1 / M}.  tile: smem scratch of Geo::TILE.
-template <int LOGN>
+// TW0 = true: tw1 also carries the per-lane twist e^{i pi l / N} (then tw1[0][l]
+// is not 1 and the caller multiplies by the lane-independent e^{i pi L m1 / N}).
+template <int LOGN, bool TW0 = false>
 __device__ __forceinline__ void fft_forward(double2 (&x)[Geo<LOGN>::P], double2* tile,
                                             const double2* tw1, int l) {
   using G = Geo<LOGN>;
   constexpr int P = G::P, L = G::L, LOGP = G::LOGP;
   dif<P, +1>(x);  // x[bitrev(k1)]
 #pragma unroll
-  for (int k1 = 1; k1 < P; ++k1) {
+  for (int k1 = TW0 ? 0 : 1; k1 < P; ++k1) {
     const int r = bitrev_c<LOGP>(k1);
     x[r] = cmul(x[r], tw1[k1 * L + l]);
   }
@@ -148,7 +152,7 @@ __device__ __forceinline__ void fft_forward(double2 (&x)[Geo<LOGN>::P], double2*
 
 // Inverse transform, exact mirror of fft_forward, scaled by M (no division):
 // In: native layout.  Out: x[m1] = M * z[L*m1 + l].
-template <int LOGN>
+template <int LOGN, bool TW0 = false>
 __device__ __forceinline__ void fft_inverse(double2 (&x)[Geo<LOGN>::P], double2* tile,
                                             const double2* tw1, int l) {
   using G = Geo<LOGN>;
@@ -177,7 +181,7 @@ __device__ __forceinline__ void fft_inverse(double2 (&x)[Geo<LOGN>::P], double2*
   for (int k1 = 0; k1 < P; ++k1) x[bitrev_c<LOGP>(k1)] = tile[k1 * L + swz(k1, l)];
   __syncwarp();
 #pragma unroll
-  for (int k1 = 1; k1 < P; ++k1) {
+  for (int k1 = TW0 ? 0 : 1; k1 < P; ++k1) {
     const int r = bitrev_c<LOGP>(k1);
     x[r] = cmulc(x[r], tw1[k1 * L + l]);
   }

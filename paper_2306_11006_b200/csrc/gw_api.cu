@@ -16,6 +16,7 @@
 
 #include "../../include/gatewave_b200.h"
 #include "blind_rotate.cuh"
+#include "br_tmem.cuh"
 #include "gates.cuh"
 #include "keyswitch.cuh"
 
@@ -61,6 +62,7 @@ struct gw_ctx {
   // wire store
   uint32_t* wires = nullptr;
   int64_t wire_slots = 0;
+  bool wires_owned = true;   // false when attached to caller memory (torch)
   // device descriptors of homogeneous gate batches, keyed by (opcode, B)
   std::map<uint64_t, BatchDesc> batch_desc;
   // timing / accounting
@@ -70,6 +72,7 @@ struct gw_ctx {
   std::vector<cudaEvent_t> ev_pool;
   int64_t prof_items[3] = {0, 0, 0};
   int64_t launches = 0;
+  int br_variant = 1;  // 1: TMEM 4-warp kernel where it fits, 0: 2-warp kernel (GATEWAVE_BR_KERNEL=v1)
   std::string err;
 };
 
@@ -151,7 +154,7 @@ int ensure_desc(gw_ctx* c, size_t bytes) {
 void host_tables(int logn, std::vector<double2>& out) {
   const int N = 1 << logn, M = N / 2;
   const int P = 1 << ((logn - 2) / 2), L = 2 * P;
-  out.resize(2 * P * L);
+  out.resize(3 * P * L);
   const long double pi = 3.141592653589793238462643383279502884L;
   for (int k1 = 0; k1 < P; ++k1)
     for (int l = 0; l < L; ++l) {
@@ -162,6 +165,12 @@ void host_tables(int logn, std::vector<double2>& out) {
     for (int l = 0; l < L; ++l) {
       long double a = pi * (long double)(L * m1 + l) / (long double)N;
       out[P * L + m1 * L + l] = make_double2((double)cosl(a), (double)sinl(a));
+    }
+  // tw1'[k1][l] = e^{i pi l (1 + 4 k1) / N}: lane twiddle with the per-lane twist folded in
+  for (int k1 = 0; k1 < P; ++k1)
+    for (int l = 0; l < L; ++l) {
+      long double a = pi * (long double)(l * (1 + 4 * k1)) / (long double)N;
+      out[2 * P * L + k1 * L + l] = make_double2((double)cosl(a), (double)sinl(a));
     }
 }
 
@@ -204,11 +213,39 @@ int launch_br_t(gw_ctx* c, const BrArgs& a0) {
   return GW_OK;
 }
 
+template <int LOGN, int LEV, int GC>
+int launch_tm_g(gw_ctx* c, const BrArgs& a0, int max_smem) {
+  BrArgs a = a0;
+  const size_t smem = TmGeo<LOGN, LEV>::smem_bytes(GC, a.n);
+  if (smem > (size_t)max_smem) return 1;  // caller falls back
+  GW_CUDA(c, cudaFuncSetAttribute(k_blind_rotate_tm<LOGN, LEV, GC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+  a.gates_per_cta = GC;
+  const int grid = (a.B + GC - 1) / GC;
+  k_blind_rotate_tm<LOGN, LEV, GC><<<grid, 128 * GC, smem, c->stream>>>(a);
+  GW_LAUNCHED(c);
+  return GW_OK;
+}
+
+// TMEM 4-warp kernel: one CTA per SM (it owns the TMEM), GC gates per CTA.
+template <int LOGN, int LEV>
+int launch_tm(gw_ctx* c, const BrArgs& a) {
+  int max_smem = 0;
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+  const int per_sm = (int)((a.B + c->sm_count - 1) / c->sm_count);
+  int rc = 1;
+  if (per_sm >= 3) rc = launch_tm_g<LOGN, LEV, 4>(c, a, max_smem);
+  if (rc == 1 && per_sm >= 2) rc = launch_tm_g<LOGN, LEV, 2>(c, a, max_smem);
+  if (rc == 1) rc = launch_tm_g<LOGN, LEV, 1>(c, a, max_smem);
+  if (rc == 1) return launch_br_t<LOGN, LEV>(c, a);
+  return rc;
+}
+
 template <int LOGN>
 int launch_br_n(gw_ctx* c, const BrArgs& a) {
   switch (c->p.l) {
-    case 1: return launch_br_t<LOGN, 1>(c, a);
-    case 2: return launch_br_t<LOGN, 2>(c, a);
+    case 1: return c->br_variant ? launch_tm<LOGN, 1>(c, a) : launch_br_t<LOGN, 1>(c, a);
+    case 2: return c->br_variant ? launch_tm<LOGN, 2>(c, a) : launch_br_t<LOGN, 2>(c, a);
     case 3: return launch_br_t<LOGN, 3>(c, a);
   }
   return fail(c, GW_ERR_PARAM, "gadget levels outside 1..3");
@@ -466,6 +503,7 @@ int gw_create(int device, gw_ctx** out) {
   if (!rc) cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
   if (!rc && (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess)) rc = GW_ERR_CUDA;
   if (!rc) rc = upload_roots(c);
+  if (const char* v = getenv("GATEWAVE_BR_KERNEL")) c->br_variant = strcmp(v, "v1") == 0 ? 0 : 1;
   if (rc) {
     gw_destroy(c);
     return rc;
@@ -486,7 +524,7 @@ int gw_destroy(gw_ctx* c) {
   cudaFree(c->acc);
   cudaFree(c->io);
   cudaFree(c->desc);
-  cudaFree(c->wires);
+  if (c->wires_owned) cudaFree(c->wires);
   for (auto& kv : c->batch_desc) cudaFree(kv.second.mem);
   if (c->desc_host) cudaFreeHost(c->desc_host);
   for (auto& v : c->prof_ev)
@@ -818,13 +856,27 @@ int gw_wires_alloc(gw_ctx* c, int64_t slots) {
   if (!c->have_params) return fail(c, GW_ERR_STATE, "parameters not set");
   cudaSetDevice(c->device);
   GW_CUDA(c, cudaStreamSynchronize(c->stream));
-  cudaFree(c->wires);
+  if (c->wires_owned) cudaFree(c->wires);
   c->wires = nullptr;
   c->wire_slots = 0;
+  c->wires_owned = true;
   if (slots == 0) return GW_OK;
   GW_CUDA(c, cudaMalloc(&c->wires, (size_t)slots * c->Wp * sizeof(uint32_t)));
   GW_CUDA(c, cudaMemsetAsync(c->wires, 0, (size_t)slots * c->Wp * sizeof(uint32_t), c->stream));
   c->wire_slots = slots;
+  return GW_OK;
+}
+
+int gw_wires_attach(gw_ctx* c, void* dev_ptr, int64_t slots, int64_t stride_words) {
+  if (!c || slots < 0 || (slots > 0 && !dev_ptr)) return GW_ERR_ARG;
+  if (!c->have_params) return fail(c, GW_ERR_STATE, "parameters not set");
+  if (stride_words != c->Wp) return fail(c, GW_ERR_DIM, "wire rows must use the engine stride (n+1 rounded up to 4)");
+  cudaSetDevice(c->device);
+  GW_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (c->wires_owned) cudaFree(c->wires);
+  c->wires = (uint32_t*)dev_ptr;
+  c->wire_slots = slots;
+  c->wires_owned = false;
   return GW_OK;
 }
 

@@ -1,0 +1,69 @@
+// tmem.cuh -- minimal tcgen05 Tensor-Memory helpers (sm_100a).
+//
+// TMEM is 128 lanes x 512 columns x 32 bit per SM.  Warp w may only touch
+// lanes [32*(w%4), 32*(w%4)+32) (its sub-partition); an address is
+// (lane << 16) | column.  We use it as a 256 KB, high-bandwidth staging
+// buffer for the bootstrapping-key slabs (never as an MMA accumulator).
+#pragma once
+#include <cstdint>
+
+namespace gw {
+
+__device__ __forceinline__ void tm_alloc(uint32_t* smem_slot, uint32_t ncols) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(smem_slot);
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(a), "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tm_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+__device__ __forceinline__ void tm_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tm_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// 32 lanes x 4 consecutive 32-bit columns: one complex double per lane.
+__device__ __forceinline__ void tm_st4(uint32_t taddr, double2 v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr),
+               "r"(__double2loint(v.x)), "r"(__double2hiint(v.x)), "r"(__double2loint(v.y)),
+               "r"(__double2hiint(v.y))
+               : "memory");
+}
+
+// 32 lanes x 16 consecutive columns: four complex doubles per lane.
+__device__ __forceinline__ void tm_ld16(uint32_t taddr, double2 (&v)[4]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+      "%13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+  tm_wait_ld();
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    v[k] = make_double2(__hiloint2double(r[4 * k + 1], r[4 * k]), __hiloint2double(r[4 * k + 3], r[4 * k + 2]));
+}
+
+// 32 lanes x 8 consecutive columns: two complex doubles per lane.
+__device__ __forceinline__ void tm_ld8(uint32_t taddr, double2 (&v)[2]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr)
+               : "memory");
+  tm_wait_ld();
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+    v[k] = make_double2(__hiloint2double(r[4 * k + 1], r[4 * k]), __hiloint2double(r[4 * k + 3], r[4 * k + 2]));
+}
+
+}  // namespace gw

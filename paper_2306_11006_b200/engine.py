@@ -34,7 +34,7 @@ EXPORTS = ("gw_version", "gw_device_count", "gw_create", "gw_destroy", "gw_last_
            "gw_set_stream", "gw_sync", "gw_set_params", "gw_upload_keys", "gw_bk_fft_size",
            "gw_download_bk_fft", "gw_blind_rotate", "gw_keyswitch", "gw_eval_gate_batch",
            "gw_eval_gate_batch_device", "gw_wires_alloc", "gw_wires_put", "gw_wires_get",
-           "gw_wires_device_ptr", "gw_plan_create", "gw_plan_run", "gw_plan_run_levels",
+           "gw_wires_device_ptr", "gw_wires_attach", "gw_plan_create", "gw_plan_run", "gw_plan_run_levels",
            "gw_plan_destroy", "gw_timer_start", "gw_timer_stop", "gw_set_profiling",
            "gw_stage_times", "gw_launch_count")
 
@@ -92,6 +92,7 @@ def load_library(path: str | None = None):
             "gw_wires_put": ([_P, _I64P, _U32P, ctypes.c_int64], ctypes.c_int),
             "gw_wires_get": ([_P, _I64P, _U32P, ctypes.c_int64], ctypes.c_int),
             "gw_wires_device_ptr": ([_P, ctypes.POINTER(_P), _I64P], ctypes.c_int),
+            "gw_wires_attach": ([_P, _P, ctypes.c_int64, ctypes.c_int64], ctypes.c_int),
             "gw_plan_create": ([_P, ctypes.c_int64, _I64P, _I32P, _I32P, _I32P,
                                 ctypes.POINTER(_P)], ctypes.c_int),
             "gw_plan_run": ([_P, _P], ctypes.c_int),
@@ -296,6 +297,14 @@ class Engine:
         stride = ctypes.c_int64(0)
         self._check(self._lib.gw_wires_device_ptr(self._ctx, ctypes.byref(p), ctypes.byref(stride)))
         return p.value or 0, stride.value
+
+    def wires_attach(self, dev_ptr: int, slots: int, stride_words: int):
+        """Use caller-owned device memory (a torch tensor) as the wire store."""
+        self._check(self._lib.gw_wires_attach(self._ctx, _P(dev_ptr), slots, stride_words))
+
+    @property
+    def row_stride(self) -> int:
+        return (self.n + 1 + 3) & ~3
 
     def plan_create(self, level_offsets, opcodes, operands, out_ids) -> "Plan":
         offs = np.ascontiguousarray(level_offsets, dtype=np.int64)

@@ -85,3 +85,42 @@ def test_config1_digest_p128(engine_mod, golden_json, golden_p128, p128_keys):
     assert digest(out) == g["out_nand"] == "6b796965e2579b67"
     assert [ctr.ntt_forward, ctr.ntt_inverse, ctr.bootstraps] == g["counters"]
     assert np.array_equal(decrypt_rows(p128_keys.lwe_sk, out), (1 - (bits_a & bits_b)).astype(np.uint8))
+
+
+@pytest.mark.parametrize("batch", [1, 150, 300, 600])
+def test_blind_rotate_batch_shapes_p128(engine_mod, p128_keys, batch):
+    """Every CTA geometry (1, 2 or 4 gates per CTA, partial last CTA) against
+    the oracle on sampled rows of random LWE samples and a random test vector."""
+    import oracle as O
+    from paper_2306_11006_b200.cggi import PARAM_128
+    rng = np.random.default_rng(batch)
+    lin = rng.integers(0, 2 ** 32, (batch, PARAM_128.n + 1), dtype=np.uint32)
+    tv = rng.integers(0, 2 ** 32, (2, PARAM_128.N), dtype=np.uint32)
+    acc = p128_keys.eval_key().engine().blind_rotate(lin, tv)
+    rows = sorted({0, batch - 1, batch // 2, batch // 3, min(batch - 1, 149), min(batch - 1, 297)})
+    okeys = O.Keys.from_params(PARAM_128, p128_keys.bootstrapping_key.data,
+                               p128_keys.keyswitch_key.data)
+    want = O.blind_rotate(lin[rows], tv, okeys.bk_ntt, PARAM_128.Bg_bits, PARAM_128.l)
+    assert np.array_equal(acc[rows], want)
+
+
+def test_two_kernel_variants_agree_p128(engine_mod, p128_keys):
+    """The 2-warp kernel (GATEWAVE_BR_KERNEL=v1) and the TMEM kernel give the
+    same accumulators (both must equal the reference; see the digest test)."""
+    import os
+    from paper_2306_11006_b200 import engine
+    from paper_2306_11006_b200.cggi import PARAM_128
+    rng = np.random.default_rng(5)
+    lin = rng.integers(0, 2 ** 32, (40, PARAM_128.n + 1), dtype=np.uint32)
+    tv = np.zeros((2, PARAM_128.N), np.uint32)
+    tv[1] = PARAM_128.mu
+    ks = p128_keys
+    a = engine.Engine(*engine.params_tuple(PARAM_128))
+    a.upload_keys(ks.bootstrapping_key.data, ks.keyswitch_key.data)
+    os.environ["GATEWAVE_BR_KERNEL"] = "v1"
+    try:
+        b = engine.Engine(*engine.params_tuple(PARAM_128))
+    finally:
+        del os.environ["GATEWAVE_BR_KERNEL"]
+    b.upload_keys(ks.bootstrapping_key.data, ks.keyswitch_key.data)
+    assert np.array_equal(a.blind_rotate(lin, tv), b.blind_rotate(lin, tv))
