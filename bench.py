@@ -118,7 +118,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.05)
+            time.sleep(0.01)
 
     def __enter__(self):
         if self._nv is not None:
@@ -146,19 +146,60 @@ def cpu_oracle_run(params, ks, A, B, threads: int):
     return out, dt
 
 
+def _load_reference():
+    """The unmodified reference package, pip-installed into baseline/_ref
+    (DESIGN.md §6); None if it is not there."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "gatewave")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/gatewave_numba_cache")
+    sys.path.insert(0, path)
+    try:
+        import gatewave.cggi  # noqa: F401
+        import gatewave.circuit  # noqa: F401
+        import gatewave.runtime  # noqa: F401
+        import gatewave.scheduler  # noqa: F401
+        return sys.modules["gatewave"]
+    except Exception:
+        return None
+
+
 def run_reference(args):
+    """Reference arm: the reference's own CPU implementation of the path on all
+    host cores -- `runtime.evaluate(gen_flat(256, NAND), build_schedule(c, K))`
+    with K = os.cpu_count() (BASELINE.md CPU-baseline plan), one full config-1
+    batch per step.  Falls back to the oracle port if baseline/_ref is absent."""
     ws, rank, _ = _dist()
     if rank != 0:
         return 0
     from paper_2306_11006_b200.cggi import PARAM_128
     model, cores = _cpu_info()
     ks, A, B, _, _ = _workload(PARAM_128, 0, args.gates)
-    for _ in range(args.warmup):
-        cpu_oracle_run(PARAM_128, ks, A, B, cores)
-    times = []
-    for _ in range(args.steps):
-        _, dt = cpu_oracle_run(PARAM_128, ks, A, B, cores)
-        times.append(dt)
+    ref = _load_reference()
+    if ref is not None:
+        from gatewave import cggi as rc, circuit as rcirc, runtime as rrt, scheduler as rsch
+        rks = rc.keygen(rc.PARAM_128, seed=7)       # same bytes as ours (tests pin the digests)
+        c = rcirc.gen_flat(args.gates, rc.GateKind.NAND)
+        sched = rsch.build_schedule(c, cores)
+        inputs = {"a": A, "b": B}
+
+        def step():
+            t0 = time.perf_counter()
+            outs, _ = rrt.evaluate(c, sched, inputs, rks)
+            return outs["y"], time.perf_counter() - t0
+        kind = "reference"
+        sample = (f"full config-1 batch ({args.gates} NAND) per step through the unmodified "
+                  f"reference (baseline/_ref gatewave.runtime.evaluate, K={cores} workers, "
+                  f"numba JIT warm) on {model}")
+    else:
+        def step():
+            return cpu_oracle_run(PARAM_128, ks, A, B, cores)
+        kind = "port"
+        sample = (f"full config-1 batch ({args.gates} NAND) per step; oracle/gw_oracle.c on "
+                  f"{cores} threads of {model} (baseline/_ref unavailable)")
+    for _ in range(max(args.warmup, 1)):
+        step()
+    times = [step()[1] for _ in range(args.steps)]
     mean = statistics.mean(times)
     value = args.gates / mean
     line = {
@@ -166,10 +207,11 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": mean * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u64 (Goldilocks NTT)", "data": "synthetic",
-        "config": {"workload": f"config1: {args.gates} independent NAND bootstraps, PARAM_128"},
-        "cpu_baseline": {"value": value, "unit": "gates/s", "cores": cores, "kind": "port",
-                         "sample": f"full config-1 batch ({args.gates} NAND) per step; "
-                                   f"oracle/gw_oracle.c on {cores} threads of {model}"},
+        "config": {"workload": f"config1: {args.gates} independent NAND gate bootstraps per GPU, "
+                               "PARAM_128 (n=630, N=1024, l=2, Bg=2^9, t=8, gamma=2)",
+                   "gates_per_gpu": args.gates},
+        "cpu_baseline": {"value": value, "unit": "gates/s", "cores": cores, "kind": kind,
+                         "sample": sample},
         "e2e": {"value": value, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
