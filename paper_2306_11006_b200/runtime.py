@@ -126,9 +126,11 @@ class LevelPlan:
     gates: int
 
 
-def compile_plan(c: Circuit, schedule: Schedule, worker: int | None = None) -> LevelPlan:
+def compile_plan(c: Circuit, schedule: Schedule, worker: int | None = None,
+                 world: int | None = None) -> LevelPlan:
     """Flatten a schedule into level arrays.  worker=None merges every worker's
-    batches into one level (single GPU); worker=k keeps rank k's slices only.
+    batches into one level (single GPU); worker=k keeps the slices of rank k,
+    i.e. batches whose worker index is k modulo `world` (default: exact match).
 
     Static SSA check over the whole schedule (the reference's per-access
     WireStore guards, runtime.py:83-96): every wire is written once, and read
@@ -154,7 +156,7 @@ def compile_plan(c: Circuit, schedule: Schedule, worker: int | None = None) -> L
     boots = 0
     for wave in schedule.waves:
         for b in wave:
-            if worker is not None and b.worker != worker:
+            if worker is not None and (b.worker % world if world else b.worker) != worker:
                 continue
             kind = as_kind(b.opcode)
             ar = GATE_ARITY[kind]

@@ -1,0 +1,98 @@
+"""Netlist evaluation on the GPU (seam 3): device wire store + level plans.
+Ciphertext outputs must equal the reference runtime's (golden adder4) and the
+oracle evaluated gate batch by gate batch; decrypted outputs equal
+simulate_plain; results are identical for every worker count."""
+import numpy as np
+import pytest
+
+from conftest import MINI
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_evaluate(c, sched, inputs, okeys, n):
+    """Reference semantics (runtime.py:122-222) with the oracle's gate batches."""
+    import oracle as O
+    rows = {}
+    for p in c.inputs:
+        for k, w in enumerate(p.wires):
+            rows[w] = inputs[p.name][k]
+    by_id = {g.id: g for g in c.gates}
+    for wave in sched.waves:
+        for b in wave:
+            gates = [by_id[gid] for gid in b.gate_ids]
+            ar = len(gates[0].operands)
+            ops = [np.stack([rows[g.operands[k]] for g in gates]) for k in range(ar)]
+            out = O.eval_gate_batch(b.opcode.value, ops, okeys, count=len(gates))
+            for g, r in zip(gates, out):
+                rows[g.id] = r
+    return {p.name: np.stack([rows[w] for w in p.wires]) for p in c.outputs}
+
+
+def test_adder4_matches_reference_runtime_mini(golden_mini, golden_json):
+    from paper_2306_11006_b200 import circuit as C
+    from paper_2306_11006_b200.cggi import EvalKey
+    from paper_2306_11006_b200.runtime import evaluate
+    from paper_2306_11006_b200.scheduler import build_schedule
+    ek = EvalKey.build(MINI, golden_mini["bk_data"], golden_mini["ksk_data"])
+    c = C.gen_adder(4)
+    outs, met = evaluate(c, build_schedule(c, 2), {"a": golden_mini["adder_a"],
+                                                   "b": golden_mini["adder_b"]}, ek)
+    assert np.array_equal(outs["s"], golden_mini["adder_s"])
+    g = golden_json["mini_adder4"]
+    assert (met.bootstrap_count, met.ntt_forward_count, met.ntt_inverse_count,
+            met.total_gates) == (g["bootstraps"], g["fwd"], g["inv"], g["total_gates"])
+    assert len(met.per_wave_wall_time) == len(g["waves"])
+
+
+@pytest.mark.parametrize("name", ["adder8", "mux3", "flat40_xor", "not_chain"])
+def test_netlists_match_oracle_and_plaintext_p128(p128_keys, name):
+    import oracle as O
+    from paper_2306_11006_b200 import circuit as C
+    from paper_2306_11006_b200.cggi import PARAM_128, GateKind, decrypt_rows, encrypt_bits
+    from paper_2306_11006_b200.rng import SeededRng
+    from paper_2306_11006_b200.runtime import evaluate
+    from paper_2306_11006_b200.scheduler import build_schedule
+    c = {"adder8": lambda: C.gen_adder(8), "mux3": lambda: C.gen_mux_tree(3),
+         "flat40_xor": lambda: C.gen_flat(40, GateKind.XOR),
+         "not_chain": lambda: C.gen_not_chain(6)}[name]()
+    rng = np.random.default_rng(80)
+    vals = {p.name: int(rng.integers(0, 1 << p.width)) for p in c.inputs}
+    srng = SeededRng(8000)
+    inputs = {p.name: encrypt_bits(PARAM_128, p128_keys.lwe_sk, C.value_to_bits(vals[p.name], p.width), srng)
+              for p in c.inputs}
+    ek = p128_keys.eval_key()
+    outs = {}
+    for K in (1, 2, 4):
+        o, met = evaluate(c, build_schedule(c, K), inputs, ek)
+        outs[K] = o
+    for K in (2, 4):
+        for k in outs[1]:
+            assert np.array_equal(outs[1][k], outs[K][k])
+    okeys = O.Keys.from_params(PARAM_128, p128_keys.bootstrapping_key.data,
+                               p128_keys.keyswitch_key.data)
+    want = _oracle_evaluate(c, build_schedule(c, 1), inputs, okeys, PARAM_128.n)
+    plain = C.simulate_plain(c, vals)
+    for k, rows in outs[1].items():
+        assert np.array_equal(rows, want[k])
+        assert C.bits_to_value(decrypt_rows(p128_keys.lwe_sk, rows)) == plain[k]
+
+
+def test_evaluate_errors(mini_keys):
+    from paper_2306_11006_b200 import circuit as C
+    from paper_2306_11006_b200.cggi import DimensionError
+    from paper_2306_11006_b200.runtime import EvaluateError, evaluate
+    from paper_2306_11006_b200.scheduler import build_schedule
+    c = C.gen_adder(2)
+    s = build_schedule(c, 1)
+    good = np.zeros((2, MINI.n + 1), np.uint32)
+    with pytest.raises(EvaluateError):
+        evaluate(c, s, {"a": good}, mini_keys)
+    with pytest.raises(EvaluateError):
+        evaluate(c, s, {"a": good, "b": good, "zz": good}, mini_keys)
+    with pytest.raises(EvaluateError):
+        evaluate(c, s, {"a": good, "b": np.zeros((3, MINI.n + 1), np.uint32)}, mini_keys)
+    with pytest.raises(DimensionError):
+        evaluate(c, s, {"a": good, "b": np.zeros((2, MINI.n), np.uint32)}, mini_keys)
+    with pytest.raises(EvaluateError):
+        evaluate(c, build_schedule(C.gen_adder(3), 1), {"a": good, "b": good}, mini_keys)
