@@ -39,11 +39,10 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
   using G = Geo<LOGN>;
   using T = TmGeo<LOGN, LEV>;
   constexpr int N = G::N, M = G::M, P = G::P, L = G::L, R = T::R, COLS = T::COLS;
-  // fill items per warp per step: its share of one (c,h) slice
+  // fill items per warp per step: its share of one (c,h) slice, streamed in
+  // three groups (issued at a phase boundary, stored at the next one)
   constexpr int ITEMS = P * R / GC;        // complex values per lane
-  constexpr int NB = 4;                    // batches per step
-  constexpr int BS = ITEMS / NB > 0 ? ITEMS / NB : 1;
-  static_assert(ITEMS % NB == 0 || ITEMS < NB, "fill batches must tile the slice");
+  constexpr int GS = (ITEMS + 2) / 3;      // items per group (register buffer)
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* tm_slot = reinterpret_cast<uint32_t*>(smem_raw);
@@ -82,35 +81,32 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
   const int32_t half_base = 1 << (a.bg_bits - 1);
 
   // ---- key-slab streaming into TMEM ----------------------------------------
-  // item t of this warp: slot s = (t / R) * GC + gl, row r = t % R
-  auto item_src = [&](int i, int t) -> const double2* {
-    const int s = (t / R) * GC + gl, r = t % R;
-    return a.bk + bk_index<LOGN, LEV>(i, co, s, r, ho, l);
-  };
-  auto item_col = [&](int buf, int t) -> uint32_t {
-    const int s = (t / R) * GC + gl, r = t % R;
-    return (uint32_t)(buf * COLS + (s * R + r) * 4);
-  };
-  double2 fb[2][BS];  // up to two batches in flight
-  auto issue = [&](int slot, int i, int batch) {
+  // item t of this warp: slot s = (t / R) * GC + gl, row r = t % R.  Offsets
+  // from the warp's (slot gl, row 0) base are compile-time constants.
+  const size_t step_stride = (size_t)2 * 2 * P * R * L;  // complex per LWE index i
+  const double2* fill_w = a.bk + bk_index<LOGN, LEV>(0, co, gl, 0, ho, l);
+  const uint32_t col_w = tm_warp + (uint32_t)(gl * R * 4);
+  double2 fb[GS];  // one group in flight
+  auto issue = [&](int i, int grp) {
+    const double2* src = fill_w + (size_t)i * step_stride;
 #pragma unroll
-    for (int k = 0; k < BS; ++k) {
-      const int t = batch * BS + k;
-      fb[slot][k] = t < ITEMS ? __ldg(item_src(i, t)) : make_double2(0.0, 0.0);
+    for (int k = 0; k < GS; ++k) {
+      const int t = grp * GS + k;
+      if (t < ITEMS) fb[k] = __ldg(src + ((t / R) * GC * R + t % R) * L);
     }
   };
-  auto store = [&](int slot, int buf, int batch) {
+  auto store = [&](int buf, int grp) {
 #pragma unroll
-    for (int k = 0; k < BS; ++k) {
-      const int t = batch * BS + k;
-      if (t < ITEMS) tm_st4(tm_warp + item_col(buf, t), fb[slot][k]);
+    for (int k = 0; k < GS; ++k) {
+      const int t = grp * GS + k;
+      if (t < ITEMS) tm_st4(col_w + (uint32_t)(buf * COLS + ((t / R) * GC * R + t % R) * 4), fb[k]);
     }
   };
 
   // prologue: slab of step 0 into buffer 0 (all gates' warps, even inactive ones)
-  for (int b = 0; b < NB; ++b) {
-    issue(0, 0, b);
-    store(0, 0, b);
+  for (int grp = 0; grp < 3; ++grp) {
+    issue(0, grp);
+    store(0, grp);
   }
   // acc <- tv * X^{-bbar} (cggi.py:612-622): warp o < 2 initialises component o
   if (active && o < 2) {
@@ -128,11 +124,11 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
   tm_fence_after();
 
   const int bar_id = 1 + gl;
-  const bool owner = lane < L;
+  const bool owner = L == 32 || lane < L;
   for (int i = 0; i < a.n; ++i) {
     const int cur = i & 1, nxt = cur ^ 1;
     const bool pre = i + 1 < a.n;
-    if (pre) issue(0, i + 1, 0);  // S0
+    if (pre) issue(i + 1, 0);  // S0
     // ---- forward: row r = o, r < R ----
     if (active && o < R) {
       const int cr = o / LEV, lv = o % LEV;
@@ -140,21 +136,22 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
       const uint32_t abar = ((lin_s[i] + radd) >> rshift) & two_n_mask;
       const int sh = 32 - (lv + 1) * a.bg_bits;
       double2 x[P];
+      const uint32_t idx0 = ((uint32_t)l - abar) & two_n_mask;
 #pragma unroll
       for (int m1 = 0; m1 < P; ++m1) {
-        int32_t d[2];
+        double dd[2];
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           const uint32_t j = (uint32_t)(L * m1 + l + hh * M);
-          const uint32_t idx = (j - abar) & two_n_mask;
+          const uint32_t idx = (idx0 + (uint32_t)(L * m1 + hh * M)) & two_n_mask;
           const uint32_t v = A[idx & (N - 1)];
-          const uint32_t rot = (idx & N) ? 0u - v : v;
-          const uint32_t buf = rot - A[j] + a.offs;
-          d[hh] = (int32_t)((buf >> sh) & base_mask) - half_base;
+          const uint32_t neg = 0u - ((idx >> LOGN) & 1u);  // all ones past X^N
+          const uint32_t buf = ((v ^ neg) - neg) - A[j] + a.offs;
+          dd[hh] = digit_to_double((buf >> sh) & base_mask, half_base);
         }
         // lane-independent part of the twist; the per-lane part lives in tw1'
-        x[m1] = cmul(make_double2(small_int_to_double(d[0]), small_int_to_double(d[1])),
-                     c_root64[G::CSTEP * m1]);
+        x[m1] = make_double2(dd[0], dd[1]);
+        if (m1 > 0) x[m1] = cmul(x[m1], c_root64[G::CSTEP * m1]);
       }
       double2* tile = xb + (size_t)o * G::TILE;
       fft_forward<LOGN, true>(x, tile, tw1, l);
@@ -163,30 +160,37 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
       for (int s = 0; s < P; ++s) tile[s * L + l] = x[s];
     }
     if (pre) {  // S1
-      store(0, nxt, 0);
-      issue(0, i + 1, 1);
+      store(nxt, 0);
+      issue(i + 1, 1);
     }
     named_barrier(bar_id, 128);
     // ---- MAC: output (co, ho) over all R rows, key from TMEM ----
     double2 acc[P];
+    constexpr int SB = GC >= 4 ? 2 : 4;  // slots per TMEM load batch (one wait per batch)
 #pragma unroll
-    for (int s = 0; s < P; ++s) {
-      double2 kr[R];
-      if constexpr (R == 4) {
-        tm_ld16(tm_warp + (uint32_t)(cur * COLS + s * R * 4), kr);
-      } else if constexpr (R == 2) {
-        tm_ld8(tm_warp + (uint32_t)(cur * COLS + s * R * 4), kr);
+    for (int s0 = 0; s0 < P; s0 += SB) {
+      uint32_t kw[SB][4 * R];
+#pragma unroll
+      for (int q = 0; q < SB; ++q)
+        tm_ld_raw<4 * R>(tm_warp + (uint32_t)(cur * COLS + (s0 + q) * R * 4), kw[q]);
+      tm_wait_ld();
+#pragma unroll
+      for (int q = 0; q < SB; ++q) {
+        const int s = s0 + q;
+        double2 sum = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const double2 kr = make_double2(__hiloint2double(kw[q][4 * r + 1], kw[q][4 * r]),
+                                          __hiloint2double(kw[q][4 * r + 3], kw[q][4 * r + 2]));
+          sum = cfma(sum, xb[(size_t)r * G::TILE + s * L + l], kr);
+        }
+        acc[s] = sum;
       }
-      double2 sum = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int r = 0; r < R; ++r) sum = cfma(sum, xb[(size_t)r * G::TILE + s * L + l], kr[r]);
-      acc[s] = sum;
     }
     named_barrier(bar_id, 128);
     if (pre) {  // S2
-      store(0, nxt, 1);
-      issue(0, i + 1, 2);
-      issue(1, i + 1, 3);
+      store(nxt, 1);
+      issue(i + 1, 2);
     }
     // ---- inverse, untwist, round, accumulate ----
     if (active) {
@@ -195,7 +199,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
       const int shift = 16 * ho;
 #pragma unroll
       for (int m1 = 0; m1 < P; ++m1) {
-        const double2 v = cmulc(acc[m1], c_root64[G::CSTEP * m1]);
+        const double2 v = m1 == 0 ? acc[0] : cmulc(acc[m1], c_root64[G::CSTEP * m1]);
         const uint32_t j = (uint32_t)(L * m1 + l);
         if (owner) {
           atomicAdd(Ac + j, round_mod32(v.x) << shift);
@@ -203,10 +207,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
         }
       }
     }
-    if (pre) {  // S3
-      store(0, nxt, 2);
-      store(1, nxt, 3);
-    }
+    if (pre) store(nxt, 2);  // S3
     tm_wait_st();
     tm_fence_before();
     __syncthreads();

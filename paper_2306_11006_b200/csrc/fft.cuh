@@ -140,9 +140,8 @@ __device__ __forceinline__ void fft_forward(double2 (&x)[Geo<LOGN>::P], double2*
     const double2 recv = shfl_xor_c(hi ? ulo : uhi, 1);
     const double2 u0 = hi ? recv : ulo;
     const double2 u1 = hi ? uhi : recv;
-    // w^c with w = e^{2 pi i / 2P}, c = j + b*P/2  ->  root64[32 j / P (+16)]
-    const double2 w = hi ? c_root64[(32 / P) * j + 16] : c_root64[(32 / P) * j];
-    const double2 t = cmul(u1, w);
+    // w^c with w = e^{2 pi i / 2P}, c = j + b*P/2: w^c = i^b * w^j (w^j lane-uniform)
+    const double2 t = mul_i_if(rot64<+1>(u1, (32 / P) * j), hi);
     y[j] = cadd(u0, t);
     y[j + P / 2] = csub(u0, t);
   }
@@ -163,8 +162,7 @@ __device__ __forceinline__ void fft_inverse(double2 (&x)[Geo<LOGN>::P], double2*
   for (int j = 0; j < P / 2; ++j) {
     const double2 X0 = x[j], X1 = x[j + P / 2];
     const double2 S = cadd(X0, X1);
-    const double2 w = hi ? c_root64[(32 / P) * j + 16] : c_root64[(32 / P) * j];
-    const double2 D = cmulc(csub(X0, X1), w);
+    const double2 D = mul_mi_if(rot64<-1>(csub(X0, X1), (32 / P) * j), hi);
     const double2 recv = shfl_xor_c(hi ? S : D, 1);
     u[bitrev_c<LOGP>(j)] = hi ? recv : S;
     u[bitrev_c<LOGP>(j + P / 2)] = hi ? D : recv;

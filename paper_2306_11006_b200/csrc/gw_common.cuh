@@ -45,6 +45,20 @@ __device__ __forceinline__ double2 cfma(double2 acc, double2 a, double2 b) {
 __device__ __forceinline__ double small_int_to_double(int32_t d) {
   return __longlong_as_double(0x4338000000000000LL + (long long)d) - 6755399441055744.0;
 }
+// (double)((int)u - half) for small u, half: the offset folds into the magic constant.
+__device__ __forceinline__ double digit_to_double(uint32_t u, int32_t half) {
+  return __longlong_as_double((long long)(0x4338000000000000LL - half) + (long long)u) - 6755399441055744.0;
+}
+// x * i^b for a lane-dependent bit b (integer sign flip + selects, no FP op).
+__device__ __forceinline__ double2 mul_i_if(double2 t, bool b) {
+  const double nty = __longlong_as_double(__double_as_longlong(t.y) ^ (long long)0x8000000000000000ULL);
+  return make_double2(b ? nty : t.x, b ? t.x : t.y);
+}
+// x * (-i)^b
+__device__ __forceinline__ double2 mul_mi_if(double2 t, bool b) {
+  const double ntx = __longlong_as_double(__double_as_longlong(t.x) ^ (long long)0x8000000000000000ULL);
+  return make_double2(b ? t.y : t.x, b ? ntx : t.y);
+}
 // Round-to-nearest integer of |x| < 2^51, returned mod 2^32.
 __device__ __forceinline__ uint32_t round_mod32(double x) {
   return (uint32_t)__double_as_longlong(__dadd_rn(x, 6755399441055744.0));

@@ -37,6 +37,27 @@ __device__ __forceinline__ void tm_st4(uint32_t taddr, double2 v) {
                : "memory");
 }
 
+// Raw 32-bit loads of NC consecutive columns, no wait (caller batches tm_wait_ld).
+template <int NC>
+__device__ __forceinline__ void tm_ld_raw(uint32_t taddr, uint32_t (&r)[NC]) {
+  if constexpr (NC == 16) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+        "%13, %14, %15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+  } else if constexpr (NC == 8) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr)
+                 : "memory");
+  } else {
+    static_assert(NC == 16 || NC == 8, "unsupported TMEM load width");
+  }
+}
+
 // 32 lanes x 16 consecutive columns: four complex doubles per lane.
 __device__ __forceinline__ void tm_ld16(uint32_t taddr, double2 (&v)[4]) {
   uint32_t r[16];
