@@ -22,7 +22,7 @@ template <int LOGN, int LEV>
 struct TmGeo {
   using G = Geo<LOGN>;
   static constexpr int R = 2 * LEV;
-  static constexpr int COLS = G::P * R * 4;  // one buffer: P slots x R rows x complex (4 cols)
+  static constexpr int COLS = G::P * R * 4;  // one buffer: [row][slot] complex (4 cols each)
   static constexpr int ALLOC = (2 * COLS) <= 32 ? 32 : (2 * COLS) <= 64 ? 64 : (2 * COLS) <= 128 ? 128
                                : (2 * COLS) <= 256 ? 256 : 512;
   static_assert(2 * COLS <= 512, "two key slabs must fit the 512 TMEM columns");
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
   // from the warp's (slot gl, row 0) base are compile-time constants.
   const size_t step_stride = (size_t)2 * 2 * P * R * L;  // complex per LWE index i
   const double2* fill_w = a.bk + bk_index<LOGN, LEV>(0, co, gl, 0, ho, l);
-  const uint32_t col_w = tm_warp + (uint32_t)(gl * R * 4);
+  const uint32_t col_w = tm_warp + (uint32_t)(gl * 4);  // slot gl of row 0
   double2 fb[GS];  // one group in flight
   auto issue = [&](int i, int grp) {
     const double2* src = fill_w + (size_t)i * step_stride;
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
 #pragma unroll
     for (int k = 0; k < GS; ++k) {
       const int t = grp * GS + k;
-      if (t < ITEMS) tm_st4(col_w + (uint32_t)(buf * COLS + ((t / R) * GC * R + t % R) * 4), fb[k]);
+      if (t < ITEMS) tm_st4(col_w + (uint32_t)(buf * COLS + ((t % R) * P + (t / R) * GC) * 4), fb[k]);
     }
   };
 
@@ -166,25 +166,24 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
     named_barrier(bar_id, 128);
     // ---- MAC: output (co, ho) over all R rows, key from TMEM ----
     double2 acc[P];
-    constexpr int SB = GC >= 4 ? 2 : 4;  // slots per TMEM load batch (one wait per batch)
+    // row-outer: the P slots are independent accumulation chains (ILP), the
+    // key row arrives 8 slots per tcgen05.ld (32 columns)
+    constexpr int SB = P < 8 ? P : 8;
 #pragma unroll
-    for (int s0 = 0; s0 < P; s0 += SB) {
-      uint32_t kw[SB][4 * R];
+    for (int r = 0; r < R; ++r) {
 #pragma unroll
-      for (int q = 0; q < SB; ++q)
-        tm_ld_raw<4 * R>(tm_warp + (uint32_t)(cur * COLS + (s0 + q) * R * 4), kw[q]);
-      tm_wait_ld();
+      for (int s0 = 0; s0 < P; s0 += SB) {
+        uint32_t kw[4 * SB];
+        tm_ld_raw<4 * SB>(tm_warp + (uint32_t)(cur * COLS + (r * P + s0) * 4), kw);
+        tm_wait_ld();
 #pragma unroll
-      for (int q = 0; q < SB; ++q) {
-        const int s = s0 + q;
-        double2 sum = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const double2 kr = make_double2(__hiloint2double(kw[q][4 * r + 1], kw[q][4 * r]),
-                                          __hiloint2double(kw[q][4 * r + 3], kw[q][4 * r + 2]));
-          sum = cfma(sum, xb[(size_t)r * G::TILE + s * L + l], kr);
+        for (int q = 0; q < SB; ++q) {
+          const int s = s0 + q;
+          const double2 kr = make_double2(__hiloint2double(kw[4 * q + 1], kw[4 * q]),
+                                          __hiloint2double(kw[4 * q + 3], kw[4 * q + 2]));
+          const double2 d = xb[(size_t)r * G::TILE + s * L + l];
+          acc[s] = r == 0 ? cmul(d, kr) : cfma(acc[s], d, kr);
         }
-        acc[s] = sum;
       }
     }
     named_barrier(bar_id, 128);
