@@ -125,6 +125,10 @@ int gw_timer_stop(gw_ctx* ctx, float* ms);
  * (bootstraps, output samples, 0) per stage: [blind_rotate, keyswitch, other]. */
 int gw_set_profiling(gw_ctx* ctx, int on);
 int gw_stage_times(gw_ctx* ctx, double* ms, int64_t* items, int reset);
+/* Debug: per-phase cycle sums of the last TMEM blind rotation, warps 0..3 of
+ * its first gate, phases [forward, fill, barrier A, MAC, inverse, step end];
+ * needs GATEWAVE_BR_PROFILE=1 at context creation. */
+int gw_br_phase_cycles(gw_ctx* ctx, long long* out);
 /* Number of engine kernel launches issued by this context so far. */
 int gw_launch_count(gw_ctx* ctx, int64_t* count);
 

@@ -26,6 +26,7 @@ struct BrArgs {
   int bg_bits;
   uint32_t offs;         // decomposition offset (cggi.py:516-522)
   int gates_per_cta;
+  long long* prof;       // optional per-phase cycle counters (debug; nullptr = off)
 };
 
 // Bootstrapping key, FFT domain: [i][c][h][s][r][lane] complex, scaled by 1/M.

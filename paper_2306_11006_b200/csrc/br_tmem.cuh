@@ -125,6 +125,17 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
 
   const int bar_id = 1 + gl;
   const bool owner = L == 32 || lane < L;
+  // phase accounting (debug): [warp o of gate 0 of CTA 0][phase] cycle sums
+  const bool prof = a.prof != nullptr && blockIdx.x == 0 && gl == 0 && lane == 0;
+  long long pt[6] = {0, 0, 0, 0, 0, 0};
+  long long tprev = clock64();
+  auto mark = [&](int ph) {
+    if (prof) {
+      const long long t = clock64();
+      pt[ph] += t - tprev;
+      tprev = t;
+    }
+  };
   for (int i = 0; i < a.n; ++i) {
     const int cur = i & 1, nxt = cur ^ 1;
     const bool pre = i + 1 < a.n;
@@ -159,11 +170,14 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
 #pragma unroll
       for (int s = 0; s < P; ++s) tile[s * L + l] = x[s];
     }
+    mark(0);
     if (pre) {  // S1
       store(nxt, 0);
       issue(i + 1, 1);
     }
+    mark(1);
     named_barrier(bar_id, 128);
+    mark(2);
     // ---- MAC: output (co, ho) over all R rows, key from TMEM ----
     double2 acc[P];
     // row-outer: the P slots are independent accumulation chains (ILP), the
@@ -186,6 +200,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
         }
       }
     }
+    mark(3);
     named_barrier(bar_id, 128);
     if (pre) {  // S2
       store(nxt, 1);
@@ -206,12 +221,16 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
         }
       }
     }
+    mark(4);
     if (pre) store(nxt, 2);  // S3
     tm_wait_st();
     tm_fence_before();
     __syncthreads();
     tm_fence_after();
+    mark(5);
   }
+  if (prof)
+    for (int ph = 0; ph < 6; ++ph) a.prof[o * 6 + ph] = pt[ph];
   if (active && o < 2) {
     uint32_t* dst = a.acc_out + ((size_t)g * 2 + o) * N;
     for (int j = lane; j < N; j += 32) dst[j] = acc_g[o * N + j];

@@ -19,6 +19,7 @@
 #include "br_tmem.cuh"
 #include "gates.cuh"
 #include "keyswitch.cuh"
+#include "ks_tc.cuh"
 
 using namespace gw;
 
@@ -46,6 +47,12 @@ struct gw_ctx {
   double2* bk_fft = nullptr;
   size_t bk_fft_count = 0;
   uint32_t* ksk = nullptr;
+  uint8_t* kimg = nullptr;     // keyswitch key as INT8 tensor-core B image (ks_tc.cuh)
+  int kt_ntiles = 0, kt_kblocks = 0;
+  bool ks_tc = false;          // tensor-core keyswitch usable for these parameters
+  int ks_variant = 1;          // 1: tensor cores when usable, 0: CUDA cores (GATEWAVE_KS_KERNEL=cuda)
+  uint32_t* ks_ut = nullptr;   // (N, count) rounded samples
+  size_t ks_ut_cap = 0;
   double2* tables = nullptr;
   uint32_t* tv_dev = nullptr;  // default test vector (0 | mu)
   // scratch
@@ -72,6 +79,7 @@ struct gw_ctx {
   std::vector<cudaEvent_t> ev_pool;
   int64_t prof_items[3] = {0, 0, 0};
   int64_t launches = 0;
+  long long* br_prof = nullptr;  // device buffer for phase cycle counters (GATEWAVE_BR_PROFILE=1)
   int br_variant = 1;  // 1: TMEM 4-warp kernel where it fits, 0: 2-warp kernel (GATEWAVE_BR_KERNEL=v1)
   std::string err;
 };
@@ -298,6 +306,44 @@ int launch_ks(gw_ctx* c, const uint32_t* acc, const KsUnit* units, int U, uint32
     k_zero_units<<<grid, 256, 0, c->stream>>>(units, U, out, out_stride, W);
     GW_LAUNCHED(c);
   }
+  if (c->ks_tc && c->ks_variant) {
+    const int N = c->p.N;
+    const size_t ut_stride = ((size_t)U + 31) & ~(size_t)31;
+    int rc = ensure(c, &c->ks_ut, &c->ks_ut_cap, ut_stride * N + ut_stride, sizeof(uint32_t));
+    if (rc) return rc;
+    uint32_t* body = c->ks_ut + ut_stride * N;
+    {
+      dim3 grid((U + 127) / 128, N);
+      k_ks_prep<<<grid, 128, 0, c->stream>>>(acc, units, U, N, c->p.ks_levels * c->p.ks_base_bits, c->ks_ut,
+                                             (int64_t)ut_stride, body);
+      GW_LAUNCHED(c);
+    }
+    KtArgs k;
+    k.ut = c->ks_ut;
+    k.ut_stride = (int64_t)ut_stride;
+    k.body = body;
+    k.units = units;
+    k.count = U;
+    k.kimg = c->kimg;
+    k.kblocks = c->kt_kblocks;
+    k.t = c->p.ks_levels;
+    k.gamma = c->p.ks_base_bits;
+    k.W = W;
+    k.out = out;
+    k.out_stride = out_stride;
+    const int mt = (U + KT_M - 1) / KT_M;
+    int splits = c->sm_count / (mt * c->kt_ntiles);
+    if (splits < 1) splits = 1;
+    if (splits > c->kt_kblocks) splits = c->kt_kblocks;
+    k.blocks_per_split = (c->kt_kblocks + splits - 1) / splits;
+    splits = (c->kt_kblocks + k.blocks_per_split - 1) / k.blocks_per_split;
+    const size_t smem = (size_t)KT_STAGES * (KT_A_BYTES + KT_B_BYTES) + 256;
+    GW_CUDA(c, cudaFuncSetAttribute(k_keyswitch_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 grid(mt, c->kt_ntiles, splits);
+    k_keyswitch_tc<<<grid, KT_THREADS, smem, c->stream>>>(k);
+    GW_LAUNCHED(c);
+    return GW_OK;
+  }
   KsArgs a;
   a.acc = acc;
   a.units = units;
@@ -396,6 +442,7 @@ int run_level(gw_ctx* c, const uint32_t* src, int64_t src_stride, uint32_t* dst,
     for (int j = 1; j <= c->p.l; ++j) off += (uint64_t)(1u << (c->p.bg_bits - 1)) << (32 - j * c->p.bg_bits);
     a.offs = (uint32_t)(off & 0xFFFFFFFFull);
     a.gates_per_cta = 1;
+    a.prof = c->br_prof;
     if ((rc = staged(c, 0, J, [&] { return launch_br(c, a); }))) return rc;
     if ((rc = staged(c, 1, U, [&] { return launch_ks(c, c->acc, units, U, dst, dst_stride); }))) return rc;
   }
@@ -504,6 +551,10 @@ int gw_create(int device, gw_ctx** out) {
   if (!rc && (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess)) rc = GW_ERR_CUDA;
   if (!rc) rc = upload_roots(c);
   if (const char* v = getenv("GATEWAVE_BR_KERNEL")) c->br_variant = strcmp(v, "v1") == 0 ? 0 : 1;
+  if (const char* v = getenv("GATEWAVE_KS_KERNEL")) c->ks_variant = strcmp(v, "cuda") == 0 ? 0 : 1;
+  if (const char* v = getenv("GATEWAVE_BR_PROFILE"))
+    if (strcmp(v, "1") == 0 && cudaMalloc(&c->br_prof, 64 * sizeof(long long)) == cudaSuccess)
+      cudaMemset(c->br_prof, 0, 64 * sizeof(long long));
   if (rc) {
     gw_destroy(c);
     return rc;
@@ -518,6 +569,9 @@ int gw_destroy(gw_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   cudaFree(c->bk_fft);
   cudaFree(c->ksk);
+  cudaFree(c->kimg);
+  cudaFree(c->ks_ut);
+  cudaFree(c->br_prof);
   cudaFree(c->tables);
   cudaFree(c->tv_dev);
   cudaFree(c->lin);
@@ -655,6 +709,20 @@ int gw_upload_keys(gw_ctx* c, const uint32_t* bk_coeff, const uint32_t* ksk) {
     GW_CUDA(c, cudaMemsetAsync(c->ksk, 0, rows * c->Wp * sizeof(uint32_t), c->stream));
     GW_CUDA(c, cudaMemcpy2DAsync(c->ksk, c->Wp * sizeof(uint32_t), ksk, (n + 1) * sizeof(uint32_t),
                                  (n + 1) * sizeof(uint32_t), rows, cudaMemcpyHostToDevice, c->stream));
+    // tensor-core image: needs t | 32 (whole digit groups per K block), <= 3 nonzero digits
+    cudaFree(c->kimg);
+    c->kimg = nullptr;
+    c->ks_tc = (32 % t == 0) && V <= 3 && ((size_t)N * t) % KT_PAIRS == 0;
+    if (c->ks_tc) {
+      c->kt_ntiles = (n + 1 + KT_COLS - 1) / KT_COLS;
+      c->kt_kblocks = (int)((size_t)N * t / KT_PAIRS);
+      const size_t bytes = (size_t)c->kt_ntiles * c->kt_kblocks * KT_B_BYTES;
+      GW_CUDA(c, cudaMalloc(&c->kimg, bytes));
+      const size_t chunks = bytes / 16;
+      k_ksk_to_tc<<<(unsigned)((chunks + 255) / 256), 256, 0, c->stream>>>(c->ksk, N, t, V, n + 1, c->Wp,
+                                                                           c->kt_ntiles, c->kt_kblocks, c->kimg);
+      GW_LAUNCHED(c);
+    }
     GW_CUDA(c, cudaStreamSynchronize(c->stream));
     c->have_ksk = true;
   }
@@ -709,6 +777,7 @@ int gw_blind_rotate(gw_ctx* c, const uint32_t* lin, int64_t B, const uint32_t* t
   for (int j = 1; j <= c->p.l; ++j) off += (uint64_t)(1u << (c->p.bg_bits - 1)) << (32 - j * c->p.bg_bits);
   a.offs = (uint32_t)(off & 0xFFFFFFFFull);
   a.gates_per_cta = 1;
+  a.prof = c->br_prof;
   if ((rc = launch_br(c, a))) return rc;
   GW_CUDA(c, cudaMemcpyAsync(acc, c->acc, (size_t)B * 2 * N * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
   GW_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -1066,6 +1135,14 @@ int gw_stage_times(gw_ctx* c, double* ms /* [3] */, int64_t* items /* [3] */, in
       c->prof_items[k] = 0;
     }
   }
+  return GW_OK;
+}
+
+int gw_br_phase_cycles(gw_ctx* c, long long* out /* [4][6] */) {
+  if (!c || !out) return GW_ERR_ARG;
+  if (!c->br_prof) return fail(c, GW_ERR_STATE, "phase profiling off (GATEWAVE_BR_PROFILE=1)");
+  GW_CUDA(c, cudaStreamSynchronize(c->stream));
+  GW_CUDA(c, cudaMemcpy(out, c->br_prof, 24 * sizeof(long long), cudaMemcpyDeviceToHost));
   return GW_OK;
 }
 

@@ -36,7 +36,7 @@ EXPORTS = ("gw_version", "gw_device_count", "gw_create", "gw_destroy", "gw_last_
            "gw_eval_gate_batch_device", "gw_wires_alloc", "gw_wires_put", "gw_wires_get",
            "gw_wires_device_ptr", "gw_wires_attach", "gw_plan_create", "gw_plan_run", "gw_plan_run_levels",
            "gw_plan_destroy", "gw_timer_start", "gw_timer_stop", "gw_set_profiling",
-           "gw_stage_times", "gw_launch_count")
+           "gw_stage_times", "gw_br_phase_cycles", "gw_launch_count")
 
 
 class EngineUnavailable(RuntimeError):
@@ -103,6 +103,7 @@ def load_library(path: str | None = None):
             "gw_set_profiling": ([_P, ctypes.c_int], ctypes.c_int),
             "gw_stage_times": ([_P, ctypes.POINTER(ctypes.c_double), _I64P, ctypes.c_int],
                                ctypes.c_int),
+            "gw_br_phase_cycles": ([_P, ctypes.POINTER(ctypes.c_longlong)], ctypes.c_int),
             "gw_launch_count": ([_P, _I64P], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
@@ -201,6 +202,13 @@ class Engine:
         self._check(self._lib.gw_stage_times(self._ctx, ms, items, 1 if reset else 0))
         names = ("blind_rotate", "keyswitch", "other")
         return {names[k]: (float(ms[k]), int(items[k])) for k in range(3)}
+
+    def br_phase_cycles(self):
+        """Debug (GATEWAVE_BR_PROFILE=1): cycles per phase for warps 0..3 of
+        the first gate of the last TMEM blind rotation."""
+        out = (ctypes.c_longlong * 24)()
+        self._check(self._lib.gw_br_phase_cycles(self._ctx, out))
+        return [[int(out[w * 6 + k]) for k in range(6)] for w in range(4)]
 
     def timer_start(self):
         self._check(self._lib.gw_timer_start(self._ctx))
