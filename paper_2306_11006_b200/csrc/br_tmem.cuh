@@ -14,6 +14,7 @@
 // FFTs; the GC warps of a sub-partition split the slice.
 #pragma once
 #include "blind_rotate.cuh"
+#include "mbarrier.cuh"
 #include "tmem.cuh"
 
 namespace gw {
@@ -28,7 +29,7 @@ struct TmGeo {
   static_assert(2 * COLS <= 512, "two key slabs must fit the 512 TMEM columns");
   static size_t smem_bytes(int gc, int n) {
     const size_t lin_words = ((size_t)n + 1 + 3) & ~(size_t)3;
-    return 16 /*tmem slot*/ + sizeof(double2) * G::TILE /*tw1'*/ +
+    return 64 /*tmem slot + mbarriers*/ + sizeof(double2) * G::TILE /*tw1'*/ +
            (size_t)gc * (sizeof(double2) * R * G::TILE + 2 * G::N * sizeof(uint32_t) +
                          lin_words * sizeof(uint32_t));
   }
@@ -46,7 +47,12 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* tm_slot = reinterpret_cast<uint32_t*>(smem_raw);
-  double2* tw1 = reinterpret_cast<double2*>(smem_raw + 16);
+  // key-slab buffer protocol: full[b] = all warps stored their share of the slab
+  // in TMEM buffer b; empty[b] = all warps finished reading buffer b (MAC)
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem_raw + 8);
+  uint64_t* empty_bar = full_bar + 2;
+  uint64_t* go_bar = full_bar + 4;
+  double2* tw1 = reinterpret_cast<double2*>(smem_raw + 64);
   double2* xbuf_all = tw1 + G::TILE;
   uint32_t* acc_all = reinterpret_cast<uint32_t*>(xbuf_all + (size_t)GC * R * G::TILE);
   const size_t lin_words = ((size_t)a.n + 1 + 3) & ~(size_t)3;
@@ -59,6 +65,14 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
   const bool active = g < a.B;
 
   for (int t = threadIdx.x; t < G::TILE; t += blockDim.x) tw1[t] = a.tables[2 * G::TILE + t];
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 2; ++k) {
+      mbar_init(&full_bar[k], 4 * GC);
+      mbar_init(&empty_bar[k], 4 * GC);
+    }
+    mbar_init(go_bar, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   if (warp == 0) tm_alloc(tm_slot, T::ALLOC);
 
   uint32_t* lin_s = lin_all + (size_t)gl * lin_words;
@@ -103,11 +117,19 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
     }
   };
 
+  // warp-level release of this warp's TMEM stores / loads to an mbarrier
+  auto release = [&](uint64_t* bar) {
+    tm_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar);
+  };
   // prologue: slab of step 0 into buffer 0 (all gates' warps, even inactive ones)
   for (int grp = 0; grp < 3; ++grp) {
     issue(0, grp);
     store(0, grp);
   }
+  tm_wait_st();
+  release(&full_bar[0]);
   // acc <- tv * X^{-bbar} (cggi.py:612-622): warp o < 2 initialises component o
   if (active && o < 2) {
     const uint32_t bbar = ((lin_s[a.n] + radd) >> rshift) & two_n_mask;
@@ -118,10 +140,11 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
       acc_g[o * N + j] = m < (uint32_t)N ? tvc[m] : 0u - tvc[m - N];
     }
   }
-  tm_wait_st();
-  tm_fence_before();
   __syncthreads();
-  tm_fence_after();
+  // stagger: odd gates start once gate 0 has finished its first forward pass,
+  // so neighbouring gates run different phases (FP64-heavy FFTs vs the
+  // shared-memory-heavy MAC) at the same time
+  if (GC > 1 && (gl & 1)) mbar_wait(go_bar, 0);
 
   const int bar_id = 1 + gl;
   const bool owner = L == 32 || lane < L;
@@ -170,13 +193,18 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
 #pragma unroll
       for (int s = 0; s < P; ++s) tile[s * L + l] = x[s];
     }
+    if (GC > 1 && i == 0 && gl == 0 && lane == 0) mbar_arrive(go_bar);
     mark(0);
-    if (pre) {  // S1
+    if (pre) {  // S1: buffer nxt is free once every warp finished MAC(i-1)
+      mbar_wait(&empty_bar[nxt], i == 0 ? 1u : (uint32_t)(((i - 1) >> 1) & 1));
+      tm_fence_after();
       store(nxt, 0);
       issue(i + 1, 1);
     }
     mark(1);
     named_barrier(bar_id, 128);
+    mbar_wait(&full_bar[cur], (uint32_t)((i >> 1) & 1));
+    tm_fence_after();
     mark(2);
     // ---- MAC: output (co, ho) over all R rows, key from TMEM ----
     double2 acc[P];
@@ -200,6 +228,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
         }
       }
     }
+    release(&empty_bar[cur]);
     mark(3);
     named_barrier(bar_id, 128);
     if (pre) {  // S2
@@ -222,11 +251,12 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
       }
     }
     mark(4);
-    if (pre) store(nxt, 2);  // S3
-    tm_wait_st();
-    tm_fence_before();
-    __syncthreads();
-    tm_fence_after();
+    if (pre) {  // S3
+      store(nxt, 2);
+      tm_wait_st();
+      release(&full_bar[nxt]);
+    }
+    named_barrier(bar_id, 128);  // acc of this gate updated before the next decomposition
     mark(5);
   }
   if (prof)
