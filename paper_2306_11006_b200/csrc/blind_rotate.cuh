@@ -27,6 +27,7 @@ struct BrArgs {
   uint32_t offs;         // decomposition offset (cggi.py:516-522)
   int gates_per_cta;
   long long* prof;       // optional per-phase cycle counters (debug; nullptr = off)
+  int ablate;            // debug timing ablations (0 = exact kernel); see br_tmem.cuh
 };
 
 // Bootstrapping key, FFT domain: [i][c][h][s][r][lane] complex, scaled by 1/M.

@@ -162,7 +162,8 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
   for (int i = 0; i < a.n; ++i) {
     const int cur = i & 1, nxt = cur ^ 1;
     const bool pre = i + 1 < a.n;
-    if (pre) issue(i + 1, 0);  // S0
+    const bool fill = pre && !(a.ablate & 4);  // debug ablation 4: no key streaming
+    if (fill) issue(i + 1, 0);  // S0
     // ---- forward: row r = o, r < R ----
     if (active && o < R) {
       const int cr = o / LEV, lv = o % LEV;
@@ -171,6 +172,10 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
       const int sh = 32 - (lv + 1) * a.bg_bits;
       double2 x[P];
       const uint32_t idx0 = ((uint32_t)l - abar) & two_n_mask;
+      if (a.ablate & 1) {  // debug: no decomposition
+#pragma unroll
+        for (int m1 = 0; m1 < P; ++m1) x[m1] = make_double2((double)(m1 + l), (double)abar);
+      } else
 #pragma unroll
       for (int m1 = 0; m1 < P; ++m1) {
         double dd[2];
@@ -188,7 +193,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
         if (m1 > 0) x[m1] = cmul(x[m1], c_root64[G::CSTEP * m1]);
       }
       double2* tile = xb + (size_t)o * G::TILE;
-      fft_forward<LOGN, true>(x, tile, tw1, l);
+      if (!(a.ablate & 16)) fft_forward<LOGN, true>(x, tile, tw1, l);
       __syncwarp();
 #pragma unroll
       for (int s = 0; s < P; ++s) tile[s * L + l] = x[s];
@@ -198,8 +203,10 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
     if (pre) {  // S1: buffer nxt is free once every warp finished MAC(i-1)
       mbar_wait(&empty_bar[nxt], i == 0 ? 1u : (uint32_t)(((i - 1) >> 1) & 1));
       tm_fence_after();
-      store(nxt, 0);
-      issue(i + 1, 1);
+      if (fill) {
+        store(nxt, 0);
+        issue(i + 1, 1);
+      }
     }
     mark(1);
     named_barrier(bar_id, 128);
@@ -211,6 +218,10 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
     // row-outer: the P slots are independent accumulation chains (ILP), the
     // key row arrives 8 slots per tcgen05.ld (32 columns)
     constexpr int SB = P < 8 ? P : 8;
+    if (a.ablate & 2) {  // debug: no MAC
+#pragma unroll
+      for (int s = 0; s < P; ++s) acc[s] = make_double2((double)s, (double)i);
+    } else
 #pragma unroll
     for (int r = 0; r < R; ++r) {
 #pragma unroll
@@ -231,20 +242,20 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
     release(&empty_bar[cur]);
     mark(3);
     named_barrier(bar_id, 128);
-    if (pre) {  // S2
+    if (fill) {  // S2
       store(nxt, 1);
       issue(i + 1, 2);
     }
     // ---- inverse, untwist, round, accumulate ----
     if (active) {
-      fft_inverse<LOGN, true>(acc, xb + (size_t)o * G::TILE, tw1, l);
+      if (!(a.ablate & 32)) fft_inverse<LOGN, true>(acc, xb + (size_t)o * G::TILE, tw1, l);
       uint32_t* Ac = acc_g + co * N;
       const int shift = 16 * ho;
 #pragma unroll
       for (int m1 = 0; m1 < P; ++m1) {
         const double2 v = m1 == 0 ? acc[0] : cmulc(acc[m1], c_root64[G::CSTEP * m1]);
         const uint32_t j = (uint32_t)(L * m1 + l);
-        if (owner) {
+        if (owner && !(a.ablate & 8)) {
           atomicAdd(Ac + j, round_mod32(v.x) << shift);
           atomicAdd(Ac + j + M, round_mod32(v.y) << shift);
         }
@@ -252,7 +263,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
     }
     mark(4);
     if (pre) {  // S3
-      store(nxt, 2);
+      if (fill) store(nxt, 2);
       tm_wait_st();
       release(&full_bar[nxt]);
     }

@@ -80,6 +80,7 @@ struct gw_ctx {
   int64_t prof_items[3] = {0, 0, 0};
   int64_t launches = 0;
   long long* br_prof = nullptr;  // device buffer for phase cycle counters (GATEWAVE_BR_PROFILE=1)
+  int br_ablate = 0;              // GATEWAVE_BR_ABLATE (debug timing only; results become wrong)
   int br_variant = 1;  // 1: TMEM 4-warp kernel where it fits, 0: 2-warp kernel (GATEWAVE_BR_KERNEL=v1)
   std::string err;
 };
@@ -443,6 +444,7 @@ int run_level(gw_ctx* c, const uint32_t* src, int64_t src_stride, uint32_t* dst,
     a.offs = (uint32_t)(off & 0xFFFFFFFFull);
     a.gates_per_cta = 1;
     a.prof = c->br_prof;
+    a.ablate = c->br_ablate;
     if ((rc = staged(c, 0, J, [&] { return launch_br(c, a); }))) return rc;
     if ((rc = staged(c, 1, U, [&] { return launch_ks(c, c->acc, units, U, dst, dst_stride); }))) return rc;
   }
@@ -552,6 +554,7 @@ int gw_create(int device, gw_ctx** out) {
   if (!rc) rc = upload_roots(c);
   if (const char* v = getenv("GATEWAVE_BR_KERNEL")) c->br_variant = strcmp(v, "v1") == 0 ? 0 : 1;
   if (const char* v = getenv("GATEWAVE_KS_KERNEL")) c->ks_variant = strcmp(v, "cuda") == 0 ? 0 : 1;
+  if (const char* v = getenv("GATEWAVE_BR_ABLATE")) c->br_ablate = atoi(v);
   if (const char* v = getenv("GATEWAVE_BR_PROFILE"))
     if (strcmp(v, "1") == 0 && cudaMalloc(&c->br_prof, 64 * sizeof(long long)) == cudaSuccess)
       cudaMemset(c->br_prof, 0, 64 * sizeof(long long));
@@ -778,6 +781,7 @@ int gw_blind_rotate(gw_ctx* c, const uint32_t* lin, int64_t B, const uint32_t* t
   a.offs = (uint32_t)(off & 0xFFFFFFFFull);
   a.gates_per_cta = 1;
   a.prof = c->br_prof;
+  a.ablate = c->br_ablate;
   if ((rc = launch_br(c, a))) return rc;
   GW_CUDA(c, cudaMemcpyAsync(acc, c->acc, (size_t)B * 2 * N * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
   GW_CUDA(c, cudaStreamSynchronize(c->stream));
