@@ -27,11 +27,13 @@ struct TmGeo {
   static constexpr int ALLOC = (2 * COLS) <= 32 ? 32 : (2 * COLS) <= 64 ? 64 : (2 * COLS) <= 128 ? 128
                                : (2 * COLS) <= 256 ? 256 : 512;
   static_assert(2 * COLS <= 512, "two key slabs must fit the 512 TMEM columns");
+  // digit exchange between the two level-warps of one accumulator component
+  static constexpr int XCHG = LEV == 2 ? 2 * 2 * (G::P / 2) * 32 : 0;  // u32 per gate
   static size_t smem_bytes(int gc, int n) {
     const size_t lin_words = ((size_t)n + 1 + 3) & ~(size_t)3;
     return 64 /*tmem slot + mbarriers*/ + sizeof(double2) * G::TILE /*tw1'*/ +
            (size_t)gc * (sizeof(double2) * R * G::TILE + 2 * G::N * sizeof(uint32_t) +
-                         lin_words * sizeof(uint32_t));
+                         lin_words * sizeof(uint32_t) + XCHG * sizeof(uint32_t));
   }
 };
 
@@ -57,6 +59,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
   uint32_t* acc_all = reinterpret_cast<uint32_t*>(xbuf_all + (size_t)GC * R * G::TILE);
   const size_t lin_words = ((size_t)a.n + 1 + 3) & ~(size_t)3;
   uint32_t* lin_all = acc_all + (size_t)GC * 2 * N;
+  uint32_t* xchg_all = lin_all + (size_t)GC * lin_words;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, l = lane & (L - 1);
   const int gl = warp >> 2, o = warp & 3;
@@ -175,6 +178,43 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
       if (a.ablate & 1) {  // debug: no decomposition
 #pragma unroll
         for (int m1 = 0; m1 < P; ++m1) x[m1] = make_double2((double)(m1 + l), (double)abar);
+      } else if constexpr (LEV == 2) {
+        // The two level-warps of component cr split the coefficients by half
+        // (warp lv takes j + lv*M), extract BOTH digit levels of their half,
+        // and swap the other level's digits through shared memory.
+        const int hh = lv;
+        const int sh_mine = sh, sh_other = 32 - (2 - lv) * a.bg_bits;
+        uint32_t* xg = xchg_all + (size_t)gl * T::XCHG + (size_t)cr * 2 * (P / 2) * 32;
+        uint32_t* to_partner = xg + (size_t)(1 - lv) * (P / 2) * 32;
+        const uint32_t* from_partner = xg + (size_t)lv * (P / 2) * 32;
+        uint32_t mine[P];
+#pragma unroll
+        for (int m1 = 0; m1 < P; m1 += 2) {
+          uint32_t oth[2];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const uint32_t j = (uint32_t)(L * (m1 + q) + l + hh * M);
+            const uint32_t idx = (idx0 + (uint32_t)(L * (m1 + q)) + (uint32_t)(hh * M)) & two_n_mask;
+            const uint32_t v = A[idx & (N - 1)];
+            const uint32_t neg = 0u - ((idx >> LOGN) & 1u);  // all ones past X^N
+            const uint32_t buf = ((v ^ neg) - neg) - A[j] + a.offs;
+            mine[m1 + q] = (buf >> sh_mine) & base_mask;
+            oth[q] = (buf >> sh_other) & base_mask;
+          }
+          to_partner[(m1 / 2) * 32 + lane] = oth[0] | (oth[1] << 16);
+        }
+        named_barrier(5 + 2 * gl + cr, 64);
+#pragma unroll
+        for (int m1 = 0; m1 < P; m1 += 2) {
+          const uint32_t w = from_partner[(m1 / 2) * 32 + lane];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const uint32_t rv = q ? (w >> 16) : (w & 0xFFFFu);
+            const uint32_t re = hh ? rv : mine[m1 + q], im = hh ? mine[m1 + q] : rv;
+            x[m1 + q] = make_double2(digit_to_double(re, half_base), digit_to_double(im, half_base));
+            if (m1 + q > 0) x[m1 + q] = cmul(x[m1 + q], c_root64[G::CSTEP * (m1 + q)]);
+          }
+        }
       } else
 #pragma unroll
       for (int m1 = 0; m1 < P; ++m1) {
