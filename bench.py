@@ -53,6 +53,7 @@ def _args():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--gates", type=int, default=GATES)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-netlist", action="store_true")
     return ap.parse_args()
 
 
@@ -218,6 +219,40 @@ def run_reference(args):
     return 0
 
 
+def config2_latency(ks, P, eng, repeats: int = 3):
+    """BASELINE configs[1]: 8-bit ripple-carry adder + 8-bit multiplier,
+    level-scheduled on one GPU through runtime.evaluate (host rows in, host
+    rows out).  Returns app latency (median over repeats) and level shapes;
+    decrypted outputs are checked against simulate_plain."""
+    from paper_2306_11006_b200 import circuit as C
+    from paper_2306_11006_b200 import netlists as NL
+    from paper_2306_11006_b200.cggi import decrypt_rows, encrypt_bits
+    from paper_2306_11006_b200.rng import SeededRng
+    from paper_2306_11006_b200.runtime import evaluate
+    from paper_2306_11006_b200.scheduler import build_schedule
+    res = {}
+    rng = np.random.default_rng(80)
+    for name, c in (("adder8", C.gen_adder(8)), ("multiplier8", NL.gen_multiplier(8))):
+        vals = {p.name: int(rng.integers(0, 1 << p.width)) for p in c.inputs}
+        srng = SeededRng(8000)
+        inputs = {p.name: encrypt_bits(P, ks.lwe_sk, C.value_to_bits(vals[p.name], p.width), srng)
+                  for p in c.inputs}
+        sched = build_schedule(c, 1)
+        evaluate(c, sched, inputs, ks)  # warm
+        lat, met, outs = [], None, None
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            outs, met = evaluate(c, sched, inputs, ks)
+            lat.append(time.perf_counter() - t0)
+        plain = C.simulate_plain(c, vals)
+        ok = all(C.bits_to_value(decrypt_rows(ks.lwe_sk, outs[k])) == v for k, v in plain.items())
+        res[name] = {"app_latency_s": statistics.median(lat), "gates": len(c.gates),
+                     "bootstraps": met.bootstrap_count, "levels": len(sched.waves),
+                     "device_time_s": met.device_time_seconds, "decrypt_ok": ok}
+    res["total_app_latency_s"] = sum(v["app_latency_s"] for v in res.values())
+    return res
+
+
 def run_ours(args):
     import torch
     ws, rank, local = _dist()
@@ -338,6 +373,11 @@ def run_ours(args):
     e2e_s = max_over_ranks(statistics.mean(e2e_times))
     parity["e2e_matches_device"] = bool(np.array_equal(r, res))
 
+    # ---- config 2 app latency: adder8 + 8-bit multiplier through evaluate() --
+    netlist = None
+    if not args.no_netlist:
+        netlist = config2_latency(ks, P, eng)
+
     # ---- CPU baseline (oracle port), rank 0 at N=1 only --------------------
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -365,6 +405,7 @@ def run_ours(args):
             "gpu_launches": launches,
             "roofline": roofline,
             "cpu_baseline": cpu,
+            "app_latency_config2": netlist,
             "clocks": clk.summary(),
             "parity": parity,
         }

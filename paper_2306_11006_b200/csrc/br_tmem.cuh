@@ -151,6 +151,14 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
 
   const int bar_id = 1 + gl;
   const bool owner = L == 32 || lane < L;
+  // lane twiddles: registers when the CTA is small enough to afford them
+  // (saves 2 x 8 KB of shared-memory reads per warp per step), else smem
+  constexpr bool TWREG = GC <= 2;
+  double2 twr[TWREG ? P : 1];
+  if constexpr (TWREG) {
+#pragma unroll
+    for (int k1 = 0; k1 < P; ++k1) twr[k1] = tw1[k1 * L + l];
+  }
   // phase accounting (debug): [warp o of gate 0 of CTA 0][phase] cycle sums
   const bool prof = a.prof != nullptr && blockIdx.x == 0 && gl == 0 && lane == 0;
   long long pt[6] = {0, 0, 0, 0, 0, 0};
@@ -233,7 +241,10 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
         if (m1 > 0) x[m1] = cmul(x[m1], c_root64[G::CSTEP * m1]);
       }
       double2* tile = xb + (size_t)o * G::TILE;
-      if (!(a.ablate & 16)) fft_forward<LOGN, true>(x, tile, tw1, l);
+      if (!(a.ablate & 16)) {
+        if constexpr (TWREG) fft_forward_tw<LOGN, true>(x, tile, TwRegs<P>{twr}, l);
+        else fft_forward<LOGN, true>(x, tile, tw1, l);
+      }
       __syncwarp();
 #pragma unroll
       for (int s = 0; s < P; ++s) tile[s * L + l] = x[s];
@@ -288,7 +299,10 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
     }
     // ---- inverse, untwist, round, accumulate ----
     if (active) {
-      if (!(a.ablate & 32)) fft_inverse<LOGN, true>(acc, xb + (size_t)o * G::TILE, tw1, l);
+      if (!(a.ablate & 32)) {
+        if constexpr (TWREG) fft_inverse_tw<LOGN, true>(acc, xb + (size_t)o * G::TILE, TwRegs<P>{twr}, l);
+        else fft_inverse<LOGN, true>(acc, xb + (size_t)o * G::TILE, tw1, l);
+      }
       uint32_t* Ac = acc_g + co * N;
       const int shift = 16 * ho;
 #pragma unroll

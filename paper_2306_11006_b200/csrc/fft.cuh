@@ -109,16 +109,43 @@ __device__ __forceinline__ int swz(int k1, int col) { return col ^ ((k1 & 3) << 
 // tw1: smem [k1][l] = e^{2 pi i l k1 / M}.  tile: smem scratch of Geo::TILE.
 // TW0 = true: tw1 also carries the per-lane twist e^{i pi l / N} (then tw1[0][l]
 // is not 1 and the caller multiplies by the lane-independent e^{i pi L m1 / N}).
+// Lane-twiddle sources: a shared-memory table [k1][lane] or a register copy.
+struct TwSmem {
+  const double2* t;
+  int L, l;
+  __device__ __forceinline__ double2 operator()(int k1) const { return t[k1 * L + l]; }
+};
+template <int P>
+struct TwRegs {
+  const double2 (&r)[P];
+  __device__ __forceinline__ double2 operator()(int k1) const { return r[k1]; }
+};
+
+template <int LOGN, bool TW0 = false, class TW>
+__device__ __forceinline__ void fft_forward_tw(double2 (&x)[Geo<LOGN>::P], double2* tile, const TW& tw, int l);
+template <int LOGN, bool TW0 = false, class TW>
+__device__ __forceinline__ void fft_inverse_tw(double2 (&x)[Geo<LOGN>::P], double2* tile, const TW& tw, int l);
+
 template <int LOGN, bool TW0 = false>
 __device__ __forceinline__ void fft_forward(double2 (&x)[Geo<LOGN>::P], double2* tile,
                                             const double2* tw1, int l) {
+  fft_forward_tw<LOGN, TW0>(x, tile, TwSmem{tw1, Geo<LOGN>::L, l}, l);
+}
+template <int LOGN, bool TW0 = false>
+__device__ __forceinline__ void fft_inverse(double2 (&x)[Geo<LOGN>::P], double2* tile,
+                                            const double2* tw1, int l) {
+  fft_inverse_tw<LOGN, TW0>(x, tile, TwSmem{tw1, Geo<LOGN>::L, l}, l);
+}
+
+template <int LOGN, bool TW0, class TW>
+__device__ __forceinline__ void fft_forward_tw(double2 (&x)[Geo<LOGN>::P], double2* tile, const TW& tw, int l) {
   using G = Geo<LOGN>;
   constexpr int P = G::P, L = G::L, LOGP = G::LOGP;
   dif<P, +1>(x);  // x[bitrev(k1)]
 #pragma unroll
   for (int k1 = TW0 ? 0 : 1; k1 < P; ++k1) {
     const int r = bitrev_c<LOGP>(k1);
-    x[r] = cmul(x[r], tw1[k1 * L + l]);
+    x[r] = cmul(x[r], tw(k1));
   }
   __syncwarp();
 #pragma unroll
@@ -151,9 +178,8 @@ __device__ __forceinline__ void fft_forward(double2 (&x)[Geo<LOGN>::P], double2*
 
 // Inverse transform, exact mirror of fft_forward, scaled by M (no division):
 // In: native layout.  Out: x[m1] = M * z[L*m1 + l].
-template <int LOGN, bool TW0 = false>
-__device__ __forceinline__ void fft_inverse(double2 (&x)[Geo<LOGN>::P], double2* tile,
-                                            const double2* tw1, int l) {
+template <int LOGN, bool TW0, class TW>
+__device__ __forceinline__ void fft_inverse_tw(double2 (&x)[Geo<LOGN>::P], double2* tile, const TW& tw, int l) {
   using G = Geo<LOGN>;
   constexpr int P = G::P, L = G::L, LOGP = G::LOGP;
   const bool hi = (l & 1) != 0;
@@ -181,7 +207,7 @@ __device__ __forceinline__ void fft_inverse(double2 (&x)[Geo<LOGN>::P], double2*
 #pragma unroll
   for (int k1 = TW0 ? 0 : 1; k1 < P; ++k1) {
     const int r = bitrev_c<LOGP>(k1);
-    x[r] = cmulc(x[r], tw1[k1 * L + l]);
+    x[r] = cmulc(x[r], tw(k1));
   }
   dit<P, -1>(x);  // x[m1]
 }
