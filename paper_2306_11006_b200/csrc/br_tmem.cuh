@@ -153,7 +153,9 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
   const bool owner = L == 32 || lane < L;
   // lane twiddles: registers when the CTA is small enough to afford them
   // (saves 2 x 8 KB of shared-memory reads per warp per step), else smem
-  constexpr bool TWREG = GC <= 2;
+  // (measured on B200: the register copy costs more than the 2 x 8 KB of smem
+  // reads it saves at GC=2 -- 4.76 vs 4.21 ms for 256 gates -- so it is off)
+  constexpr bool TWREG = false;
   double2 twr[TWREG ? P : 1];
   if constexpr (TWREG) {
 #pragma unroll
