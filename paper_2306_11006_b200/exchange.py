@@ -89,6 +89,23 @@ class _DeviceLevels:
         self.eng.wires_alloc(0)
 
 
+def _all_gather(send, world: int, group):
+    """all_gather of equal-size row blocks.  NCCL takes device tensors
+    directly (NVLink); a CPU backend (gloo, used by the one-GPU two-rank test)
+    gets a host-staged copy."""
+    import torch
+    import torch.distributed as dist
+    backend = dist.get_backend(group)
+    if send.is_cuda and backend != "nccl":
+        host = send.cpu()
+        out = torch.empty((world * host.shape[0], host.shape[1]), dtype=host.dtype)
+        dist.all_gather_into_tensor(out, host, group=group)
+        return out.to(send.device)
+    out = torch.empty((world * send.shape[0], send.shape[1]), dtype=send.dtype, device=send.device)
+    dist.all_gather_into_tensor(out, send, group=group)
+    return out
+
+
 def evaluate_distributed(c: Circuit, schedule: Schedule, mats: dict, ek: EvalKey, *, group=None,
                          levels_factory=None):
     """Rank-local part of `runtime.evaluate` for world > 1.
@@ -128,8 +145,7 @@ def evaluate_distributed(c: Circuit, schedule: Schedule, mats: dict, ek: EvalKey
                 send = torch.zeros((m, wires.shape[1]), dtype=torch.int32, device=device)
                 if len(mine):
                     send[:len(mine)] = wires[torch.as_tensor(mine, device=device)]
-                recv = torch.empty((world * m, wires.shape[1]), dtype=torch.int32, device=device)
-                dist.all_gather_into_tensor(recv, send, group=group)
+                recv = _all_gather(send, world, group)
                 for q in range(world):
                     ids = xplan.sends[L][q]
                     if q == rank or not len(ids):

@@ -1,0 +1,71 @@
+"""Two ranks on one B200 (gloo process group, host-staged exchange): the real
+CUDA engine runs each rank's level slices and the cross-rank wire exchange
+must reproduce the single-process ciphertexts bit for bit."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from conftest import MINI
+
+pytestmark = pytest.mark.gpu
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2306_11006_b200 import circuit as C
+    from paper_2306_11006_b200 import netlists as NL
+    from paper_2306_11006_b200.cggi import EvalKey, encrypt_bits, keygen
+    from paper_2306_11006_b200.rng import SeededRng
+    from paper_2306_11006_b200.runtime import evaluate
+    from paper_2306_11006_b200.scheduler import build_schedule
+    ks = keygen(MINI, 2024)
+    res = []
+    for c in (C.gen_adder(4), NL.gen_multiplier(4), C.gen_mux_tree(2)):
+        rng = np.random.default_rng(3)
+        srng = SeededRng(11)
+        inputs = {p.name: encrypt_bits(MINI, ks.lwe_sk, rng.integers(0, 2, p.width), srng) for p in c.inputs}
+        outs, met = evaluate(c, build_schedule(c, world), inputs, ks)
+        res.append({k: v.tobytes() for k, v in outs.items()})
+    q.put((rank, res))
+    dist.destroy_process_group()
+
+
+def _single():
+    from paper_2306_11006_b200 import circuit as C
+    from paper_2306_11006_b200 import netlists as NL
+    from paper_2306_11006_b200.cggi import encrypt_bits, keygen
+    from paper_2306_11006_b200.rng import SeededRng
+    from paper_2306_11006_b200.runtime import evaluate
+    from paper_2306_11006_b200.scheduler import build_schedule
+    ks = keygen(MINI, 2024)
+    res = []
+    for c in (C.gen_adder(4), NL.gen_multiplier(4), C.gen_mux_tree(2)):
+        rng = np.random.default_rng(3)
+        srng = SeededRng(11)
+        inputs = {p.name: encrypt_bits(MINI, ks.lwe_sk, rng.integers(0, 2, p.width), srng) for p in c.inputs}
+        outs, _ = evaluate(c, build_schedule(c, 1), inputs, ks)
+        res.append({k: v.tobytes() for k, v in outs.items()})
+    return res
+
+
+def test_two_ranks_one_gpu_match_single_process():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    want = _single()
+    assert got[0] == want and got[1] == want
