@@ -162,9 +162,10 @@ def evaluate_distributed(c: Circuit, schedule: Schedule, mats: dict, ek: EvalKey
     finally:
         lv.close()
     # whole-job metrics: wall time is the max over ranks
-    t = torch.tensor([t1 - t0] + per_wave, dtype=torch.float64, device=device)
+    cdev = device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    t = torch.tensor([t1 - t0] + per_wave, dtype=torch.float64, device=cdev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
-    boots = torch.tensor([plan.bootstraps], dtype=torch.int64, device=device)
+    boots = torch.tensor([plan.bootstraps], dtype=torch.int64, device=cdev)
     dist.all_reduce(boots, group=group)
     total_boot = int(boots.item())
     m = Metrics(total_gates=len(c.gates), workers=schedule.workers, gpus=world)
