@@ -29,25 +29,26 @@ static inline uint64_t mm(uint64_t a, uint64_t b) {
   u128 p = (u128)a * b;
   uint64_t lo = (uint64_t)p, hi = (uint64_t)(p >> 64);
   uint64_t h_hi = hi >> 32, h_lo = hi & M32;
+  /* same arithmetic as the reference, written branch-free (conditional moves) */
   uint64_t t = lo - h_hi;
-  if (lo < h_hi) t -= M32;
+  t -= (uint64_t)(lo < h_hi) * M32;
   uint64_t u = (h_lo << 32) - h_lo;
   uint64_t s = t + u;
-  if (s < t) s += M32;
-  if (s >= Q) s -= Q;
+  s += (uint64_t)(s < t) * M32;
+  s -= (uint64_t)(s >= Q) * Q;
   return s;
 }
 /* torus.py:91-98 (_ma) */
 static inline uint64_t ma(uint64_t a, uint64_t b) {
   uint64_t s = a + b;
-  if (s < a) s += M32;
-  if (s >= Q) s -= Q;
+  s += (uint64_t)(s < a) * M32;
+  s -= (uint64_t)(s >= Q) * Q;
   return s;
 }
 /* torus.py:101-106 (_ms) */
 static inline uint64_t ms(uint64_t a, uint64_t b) {
   uint64_t d = a - b;
-  if (a < b) d -= M32;
+  d -= (uint64_t)(a < b) * M32;
   return d;
 }
 
@@ -197,88 +198,88 @@ uint32_t orc_decompose_offset(int bg_bits, int levels) {
 }
 
 /*
- * cggi.py:592-667 (_blind_rotate_kernel) for one gate.  The reference loops
- * i outer / gate inner for cache reuse; every gate is independent, so the
- * per-gate order used here (and parallelised over gates) gives identical bits.
+ * cggi.py:592-667 (_blind_rotate_kernel), same loop order as the reference:
+ * LWE index i outermost, gates inner, so the 64 KB NTT-domain key slice
+ * BK_i stays cache-resident across the batch.  Each worker thread owns a
+ * contiguous chunk of gates (results do not depend on the split).
  */
-static void blind_rotate_one(const uint32_t* ct, int n, const uint32_t* tv, int N, int log_n,
-                             const uint64_t* bk_ntt, int bg_bits, int levels,
-                             const uint64_t* psi_brv, const uint64_t* ipsi_brv, uint64_t n_inv,
-                             uint32_t* acc /* (2,N) */, uint64_t* resid /* (2l,N) */,
-                             uint64_t* accntt /* (2,N) */) {
+typedef struct {
+  const uint32_t* cts; int64_t B; int n; const uint32_t* tv; int N; int log_n; const uint64_t* bk_ntt;
+  int bg_bits; int levels; const uint64_t* psi_brv; const uint64_t* ipsi_brv; uint64_t n_inv;
+  uint32_t* acc_out; int threads;
+} br_args;
+
+static void br_chunk(void* ctx, int64_t chunk, void* scratch) {
+  br_args* a = (br_args*)ctx;
+  const int N = a->N, n = a->n, levels = a->levels, bg_bits = a->bg_bits;
   const int two_n = 2 * N, rows = 2 * levels;
-  const uint64_t rshift = 32 - (log_n + 1);
-  const uint64_t radd = 1ULL << (32 - (log_n + 1) - 1);
+  const int64_t per = (a->B + a->threads - 1) / a->threads;
+  const int64_t g0 = chunk * per, g1 = g0 + per < a->B ? g0 + per : a->B;
+  if (g0 >= g1) return;
+  uint64_t* resid = (uint64_t*)scratch;
+  uint64_t* accntt = resid + (size_t)rows * N;
+  const uint64_t rshift = 32 - (a->log_n + 1);
+  const uint64_t radd = 1ULL << (32 - (a->log_n + 1) - 1);
   const uint64_t base_mask = (1ULL << bg_bits) - 1;
   const int64_t half_base = 1LL << (bg_bits - 1);
   const uint64_t offs = orc_decompose_offset(bg_bits, levels);
   const uint64_t two32 = 1ULL << 32;
   const uint64_t qhalf = Q / 2;
-
   /* :612-622 acc <- tv * X^{-bbar} */
-  int bbar = (int)((((uint64_t)ct[n]) + radd) >> rshift) & (two_n - 1);
-  int k = (two_n - bbar) & (two_n - 1);
-  for (int c = 0; c < 2; ++c)
-    for (int j = 0; j < N; ++j) {
-      int m = (j - k) & (two_n - 1);
-      acc[c * N + j] = m < N ? tv[c * N + m] : (uint32_t)((two32 - tv[c * N + m - N]) & M32);
-    }
-
-  for (int i = 0; i < n; ++i) {
-    const uint64_t* bk_i = bk_ntt + (size_t)i * rows * 2 * N;
-    int abar = (int)((((uint64_t)ct[i]) + radd) >> rshift) & (two_n - 1);
-    /* :629-644 rotate-subtract + decompose into residues */
-    for (int c = 0; c < 2; ++c) {
-      const uint32_t* row = acc + c * N;
+  for (int64_t g = g0; g < g1; ++g) {
+    const uint32_t* ct = a->cts + g * (n + 1);
+    uint32_t* acc = a->acc_out + g * 2 * N;
+    int bbar = (int)((((uint64_t)ct[n]) + radd) >> rshift) & (two_n - 1);
+    int k = (two_n - bbar) & (two_n - 1);
+    for (int c = 0; c < 2; ++c)
       for (int j = 0; j < N; ++j) {
-        int m = (j - abar) & (two_n - 1);
-        uint64_t rot = m < N ? (uint64_t)row[m] : ((two32 - (uint64_t)row[m - N]) & M32);
-        uint64_t buf = ((rot - (uint64_t)row[j]) + offs) & M32;
-        for (int lv = 0; lv < levels; ++lv) {
-          uint64_t sh = 32 - (lv + 1) * bg_bits;
-          int64_t dig = (int64_t)((buf >> sh) & base_mask) - half_base;
-          resid[(c * levels + lv) * N + j] = dig < 0 ? Q + (uint64_t)dig : (uint64_t)dig;
+        int m = (j - k) & (two_n - 1);
+        acc[c * N + j] = m < N ? a->tv[c * N + m] : (uint32_t)((two32 - a->tv[c * N + m - N]) & M32);
+      }
+  }
+  for (int i = 0; i < n; ++i) {
+    const uint64_t* bk_i = a->bk_ntt + (size_t)i * rows * 2 * N;
+    for (int64_t g = g0; g < g1; ++g) {
+      uint32_t* acc = a->acc_out + g * 2 * N;
+      int abar = (int)((((uint64_t)a->cts[g * (n + 1) + i]) + radd) >> rshift) & (two_n - 1);
+      /* :627-644 rotate-subtract + decompose into residues */
+      for (int c = 0; c < 2; ++c) {
+        const uint32_t* row = acc + c * N;
+        for (int j = 0; j < N; ++j) {
+          int m = (j - abar) & (two_n - 1);
+          uint64_t rot = m < N ? (uint64_t)row[m] : ((two32 - (uint64_t)row[m - N]) & M32);
+          uint64_t buf = ((rot - (uint64_t)row[j]) + offs) & M32;
+          for (int lv = 0; lv < levels; ++lv) {
+            uint64_t sh = 32 - (lv + 1) * bg_bits;
+            int64_t dig = (int64_t)((buf >> sh) & base_mask) - half_base;
+            resid[(c * levels + lv) * N + j] = dig < 0 ? Q + (uint64_t)dig : (uint64_t)dig;
+          }
+        }
+      }
+      /* :645-647 forward transforms */
+      for (int r = 0; r < rows; ++r) ntt_fwd(resid + r * N, N, a->psi_brv);
+      /* :648-657 MAC against the TGSW rows */
+      memset(accntt, 0, sizeof(uint64_t) * 2 * N);
+      for (int r = 0; r < rows; ++r)
+        for (int c2 = 0; c2 < 2; ++c2) {
+          const uint64_t* bkrow = bk_i + ((size_t)r * 2 + c2) * N;
+          uint64_t* arow = accntt + c2 * N;
+          const uint64_t* dr = resid + r * N;
+          for (int j = 0; j < N; ++j) arow[j] = ma(arow[j], mm(dr[j], bkrow[j]));
+        }
+      /* :658-666 inverse + accumulate */
+      for (int c2 = 0; c2 < 2; ++c2) {
+        uint64_t* arow = accntt + c2 * N;
+        ntt_inv(arow, N, a->ipsi_brv, a->n_inv);
+        uint32_t* out = acc + c2 * N;
+        for (int j = 0; j < N; ++j) {
+          uint64_t rr = arow[j];
+          uint64_t tor = ((rr & M32) - (rr > qhalf ? 1ULL : 0ULL)) & M32;
+          out[j] = (uint32_t)(((uint64_t)out[j] + tor) & M32);
         }
       }
     }
-    /* :645-647 forward transforms */
-    for (int r = 0; r < rows; ++r) ntt_fwd(resid + r * N, N, psi_brv);
-    /* :648-657 MAC against the TGSW rows */
-    memset(accntt, 0, sizeof(uint64_t) * 2 * N);
-    for (int r = 0; r < rows; ++r)
-      for (int c2 = 0; c2 < 2; ++c2) {
-        const uint64_t* bkrow = bk_i + ((size_t)r * 2 + c2) * N;
-        uint64_t* arow = accntt + c2 * N;
-        const uint64_t* dr = resid + r * N;
-        for (int j = 0; j < N; ++j) arow[j] = ma(arow[j], mm(dr[j], bkrow[j]));
-      }
-    /* :658-666 inverse + accumulate */
-    for (int c2 = 0; c2 < 2; ++c2) {
-      uint64_t* arow = accntt + c2 * N;
-      ntt_inv(arow, N, ipsi_brv, n_inv);
-      uint32_t* out = acc + c2 * N;
-      for (int j = 0; j < N; ++j) {
-        uint64_t rr = arow[j];
-        uint64_t tor = ((rr & M32) - (rr > qhalf ? 1ULL : 0ULL)) & M32;
-        out[j] = (uint32_t)(((uint64_t)out[j] + tor) & M32);
-      }
-    }
   }
-}
-
-typedef struct {
-  const uint32_t* cts; int n; const uint32_t* tv; int N; int log_n; const uint64_t* bk_ntt;
-  int bg_bits; int levels; const uint64_t* psi_brv; const uint64_t* ipsi_brv; uint64_t n_inv;
-  uint32_t* acc_out;
-} br_args;
-
-static void br_task(void* ctx, int64_t g, void* scratch) {
-  br_args* a = (br_args*)ctx;
-  uint64_t* resid = (uint64_t*)scratch;
-  uint64_t* accntt = resid + 2 * a->levels * a->N;
-  blind_rotate_one(a->cts + g * (a->n + 1), a->n, a->tv, a->N, a->log_n, a->bk_ntt, a->bg_bits,
-                   a->levels, a->psi_brv, a->ipsi_brv, a->n_inv, a->acc_out + g * 2 * a->N,
-                   resid, accntt);
 }
 
 int orc_blind_rotate(const uint32_t* cts, int64_t B, int n, const uint32_t* tv, int N,
@@ -287,9 +288,11 @@ int orc_blind_rotate(const uint32_t* cts, int64_t B, int n, const uint32_t* tv, 
   int log_n = 0;
   while ((1 << log_n) < N) ++log_n;
   if ((1 << log_n) != N) return -1;
-  br_args a = {cts, n, tv, N, log_n, bk_ntt, bg_bits, levels, psi_brv, ipsi_brv, n_inv, acc_out};
+  if (threads < 1) threads = 1;
+  if (threads > B) threads = (int)(B > 0 ? B : 1);
+  br_args a = {cts, B, n, tv, N, log_n, bk_ntt, bg_bits, levels, psi_brv, ipsi_brv, n_inv, acc_out, threads};
   size_t scratch = sizeof(uint64_t) * (size_t)(2 * levels * N + 2 * N);
-  return orc_parallel_for(B, threads, scratch, br_task, &a);
+  return orc_parallel_for(threads, threads, scratch, br_chunk, &a);
 }
 
 /* cggi.py:695-704 (_extract_rows) */
