@@ -101,31 +101,22 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
   // item t of this warp: slot s = (t / R) * GC + gl, row r = t % R.  Offsets
   // from the warp's (slot gl, row 0) base are compile-time constants.
   const size_t step_stride = (size_t)2 * 2 * P * R * L;  // complex per LWE index i
-  // Sub-partition o = (co, ho) holds, per buffer, columns [r][which][k]: the
-  // key of its own output (which 0: (co, ho)) and of its h-partner's output
-  // (which 1: (co, 1-ho)) at the P/2 slots s = ho*P/2 + k it MACs.  The GC
-  // warps of the sub-partition fill consecutive column ranges.
-  constexpr int HP = P / 2;
-  const double2* fill_own = a.bk + bk_index<LOGN, LEV>(0, co, ho * HP, 0, ho, l);
-  const double2* fill_par = a.bk + bk_index<LOGN, LEV>(0, co, ho * HP, 0, 1 - ho, l);
-  const int t0 = gl * ITEMS;
+  const double2* fill_w = a.bk + bk_index<LOGN, LEV>(0, co, gl, 0, ho, l);
+  const uint32_t col_w = tm_warp + (uint32_t)(gl * 4);  // slot gl of row 0
   double2 fb[GS];  // one group in flight
   auto issue = [&](int i, int grp) {
+    const double2* src = fill_w + (size_t)i * step_stride;
 #pragma unroll
     for (int k = 0; k < GS; ++k) {
-      const int t = t0 + grp * GS + k;  // column index / 4 = (r*2 + which)*HP + kk
-      if (grp * GS + k < ITEMS) {
-        const int r = t / P, which = (t / HP) & 1, kk = t % HP;
-        const double2* src = (which ? fill_par : fill_own) + (size_t)i * step_stride;
-        fb[k] = __ldg(src + (size_t)(kk * R + r) * L);
-      }
+      const int t = grp * GS + k;
+      if (t < ITEMS) fb[k] = __ldg(src + ((t / R) * GC * R + t % R) * L);
     }
   };
   auto store = [&](int buf, int grp) {
 #pragma unroll
     for (int k = 0; k < GS; ++k) {
-      const int t = t0 + grp * GS + k;
-      if (grp * GS + k < ITEMS) tm_st4(tm_warp + (uint32_t)(buf * COLS + t * 4), fb[k]);
+      const int t = grp * GS + k;
+      if (t < ITEMS) tm_st4(col_w + (uint32_t)(buf * COLS + ((t % R) * P + (t / R) * GC) * 4), fb[k]);
     }
   };
 
@@ -277,50 +268,33 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
     mark(2);
     // ---- MAC: output (co, ho) over all R rows, key from TMEM ----
     double2 acc[P];
-    // Slot-split MAC: the h-pair (co, 0)/(co, 1) share all D^ reads by each
-    // taking half the slots (ho*P/2 ..) for BOTH outputs of component co, then
-    // trading the half that belongs to the partner's output.
-    double2 own[HP], par[HP];
+    // row-outer: the P slots are independent accumulation chains (ILP), the
+    // key row arrives 8 slots per tcgen05.ld (32 columns)
+    constexpr int SB = P < 8 ? P : 8;
     if (a.ablate & 2) {  // debug: no MAC
 #pragma unroll
-      for (int k = 0; k < HP; ++k) own[k] = par[k] = make_double2((double)k, (double)i);
+      for (int s = 0; s < P; ++s) acc[s] = make_double2((double)s, (double)i);
     } else
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const double2* drow = xb + (size_t)r * G::TILE + (size_t)(ho * HP) * L + l;
-      double2 d[HP];
 #pragma unroll
-      for (int k = 0; k < HP; ++k) d[k] = drow[k * L];
-#pragma unroll
-      for (int which = 0; which < 2; ++which) {
-        uint32_t kw[4 * HP];  // key of row r for output `which`, slots k
-        tm_ld_raw<4 * HP>(tm_warp + (uint32_t)(cur * COLS + ((r * 2 + which) * HP) * 4), kw);
+      for (int s0 = 0; s0 < P; s0 += SB) {
+        uint32_t kw[4 * SB];
+        tm_ld_raw<4 * SB>(tm_warp + (uint32_t)(cur * COLS + (r * P + s0) * 4), kw);
         tm_wait_ld();
 #pragma unroll
-        for (int k = 0; k < HP; ++k) {
-          const double2 kk = make_double2(__hiloint2double(kw[4 * k + 1], kw[4 * k]),
-                                          __hiloint2double(kw[4 * k + 3], kw[4 * k + 2]));
-          double2& dst = which ? par[k] : own[k];
-          dst = r == 0 ? cmul(d[k], kk) : cfma(dst, d[k], kk);
+        for (int q = 0; q < SB; ++q) {
+          const int s = s0 + q;
+          const double2 kr = make_double2(__hiloint2double(kw[4 * q + 1], kw[4 * q]),
+                                          __hiloint2double(kw[4 * q + 3], kw[4 * q + 2]));
+          const double2 d = xb[(size_t)r * G::TILE + s * L + l];
+          acc[s] = r == 0 ? cmul(d, kr) : cfma(acc[s], d, kr);
         }
       }
     }
     release(&empty_bar[cur]);
     mark(3);
-    named_barrier(bar_id, 128);  // every D^ read of this gate done: xb is free
-    {
-      double2* to_partner = xb + (size_t)(o ^ 1) * G::TILE + l;
-#pragma unroll
-      for (int k = 0; k < HP; ++k) to_partner[k * L] = par[k];
-      named_barrier(5 + 2 * gl + co, 64);
-      const double2* from_partner = xb + (size_t)o * G::TILE + l;
-#pragma unroll
-      for (int k = 0; k < HP; ++k) {
-        const double2 rv = from_partner[k * L];
-        acc[k] = ho ? rv : own[k];
-        acc[HP + k] = ho ? own[k] : rv;
-      }
-    }
+    named_barrier(bar_id, 128);
     if (fill) {  // S2
       store(nxt, 1);
       issue(i + 1, 2);

@@ -58,18 +58,13 @@ __device__ __forceinline__ void tm_ld_raw(uint32_t taddr, uint32_t (&r)[NC]) {
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr)
         : "memory");
-  } else if constexpr (NC == 4) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                 : "r"(taddr)
-                 : "memory");
   } else if constexpr (NC == 8) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                  : "r"(taddr)
                  : "memory");
   } else {
-    static_assert(NC == 32 || NC == 16 || NC == 8 || NC == 4, "unsupported TMEM load width");
+    static_assert(NC == 32 || NC == 16 || NC == 8, "unsupported TMEM load width");
   }
 }
 
