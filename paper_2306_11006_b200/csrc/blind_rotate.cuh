@@ -127,7 +127,8 @@ __global__ void __launch_bounds__(256, 1) k_blind_rotate(BrArgs a) {
           dg[hh][lv] = (int32_t)((buf >> (32 - (lv + 1) * a.bg_bits)) & base_mask) - half_base;
       }
       const double2 tw = twist[m1 * L + l];
-      x[m1] = cmul(make_double2(small_int_to_double(dg[0][0]), small_int_to_double(dg[1][0])), tw);
+      x[bitrev_c<G::LOGP>(m1)] =
+          cmul(make_double2(small_int_to_double(dg[0][0]), small_int_to_double(dg[1][0])), tw);
 #pragma unroll
       for (int lv = 1; lv < LEV; ++lv)
         packed[lv - 1][m1] = ((uint32_t)dg[0][lv] & 0xFFFFu) | ((uint32_t)dg[1][lv] << 16);
@@ -141,8 +142,8 @@ __global__ void __launch_bounds__(256, 1) k_blind_rotate(BrArgs a) {
           const uint32_t pk = packed[lv - 1][m1];
           const int32_t d0 = (int32_t)(int16_t)(pk & 0xFFFFu);
           const int32_t d1 = (int32_t)pk >> 16;
-          x[m1] = cmul(make_double2(small_int_to_double(d0), small_int_to_double(d1)),
-                       twist[m1 * L + l]);
+          x[bitrev_c<G::LOGP>(m1)] = cmul(make_double2(small_int_to_double(d0), small_int_to_double(d1)),
+                                          twist[m1 * L + l]);
         }
       }
       fft_forward<LOGN>(x, tile, tw1, l);
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(128) k_bk_to_fft(const uint32_t* __restrict__ 
       const int32_t lo = (int32_t)(int16_t)(w & 0xFFFF);
       part[hh] = h == 0 ? lo : (int32_t)(((int64_t)w - lo) >> 16);
     }
-    x[m1] = cmul(make_double2((double)part[0], (double)part[1]), twist[m1 * L + l]);
+    x[bitrev_c<G::LOGP>(m1)] = cmul(make_double2((double)part[0], (double)part[1]), twist[m1 * L + l]);
   }
   fft_forward<LOGN>(x, tiles[warp], tw1, l);
   const double scale = 1.0 / (double)M;

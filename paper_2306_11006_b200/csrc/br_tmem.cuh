@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
       const uint32_t idx0 = ((uint32_t)l - abar) & two_n_mask;
       if (a.ablate & 1) {  // debug: no decomposition
 #pragma unroll
-        for (int m1 = 0; m1 < P; ++m1) x[m1] = make_double2((double)(m1 + l), (double)abar);
+        for (int m1 = 0; m1 < P; ++m1) x[bitrev_c<G::LOGP>(m1)] = make_double2((double)(m1 + l), (double)abar);
       } else if constexpr (LEV == 2) {
         // The two level-warps of component cr split the coefficients by half
         // (warp lv takes j + lv*M), extract BOTH digit levels of their half,
@@ -221,8 +221,9 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
           for (int q = 0; q < 2; ++q) {
             const uint32_t rv = q ? (w >> 16) : (w & 0xFFFFu);
             const uint32_t re = hh ? rv : mine[m1 + q], im = hh ? mine[m1 + q] : rv;
-            x[m1 + q] = make_double2(digit_to_double(re, half_base), digit_to_double(im, half_base));
-            if (m1 + q > 0) x[m1 + q] = cmul(x[m1 + q], c_root64[G::CSTEP * (m1 + q)]);
+            double2 v = make_double2(digit_to_double(re, half_base), digit_to_double(im, half_base));
+            if (m1 + q > 0) v = cmul(v, c_root64[G::CSTEP * (m1 + q)]);
+            x[bitrev_c<G::LOGP>(m1 + q)] = v;  // DIT forward takes bit-reversed input
           }
         }
       } else
@@ -239,8 +240,9 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
           dd[hh] = digit_to_double((buf >> sh) & base_mask, half_base);
         }
         // lane-independent part of the twist; the per-lane part lives in tw1'
-        x[m1] = make_double2(dd[0], dd[1]);
-        if (m1 > 0) x[m1] = cmul(x[m1], c_root64[G::CSTEP * m1]);
+        double2 v = make_double2(dd[0], dd[1]);
+        if (m1 > 0) v = cmul(v, c_root64[G::CSTEP * m1]);
+        x[bitrev_c<G::LOGP>(m1)] = v;
       }
       double2* tile = xb + (size_t)o * G::TILE;
       if (!(a.ablate & 16)) {

@@ -67,18 +67,49 @@ __device__ __forceinline__ void dif_stage(double2 (&x)[P]) {
   }
 }
 
+// DIT butterfly (a, b) <- (a + w b, a - w b), w = e^{SIGN 2 pi i t / 64}.
+// Non-trivial twiddles use the tangent form w = s (1 + i r) (or s (r + i)),
+// |r| <= 1: 6 FP64 ops instead of 8 (complex multiply + two complex adds).
+template <int SIGN>
+__device__ __forceinline__ void bfly(double2& a, double2& b, int t) {
+  if (t == 0) {
+    const double2 s = cadd(a, b), d = csub(a, b);
+    a = s;
+    b = d;
+    return;
+  }
+  if (t == 16) {  // w = SIGN * i
+    const double2 wb = SIGN > 0 ? make_double2(-b.y, b.x) : make_double2(b.y, -b.x);
+    const double2 s = cadd(a, wb), d = csub(a, wb);
+    a = s;
+    b = d;
+    return;
+  }
+  const double2 cs = c_ts64[t];
+  const bool case_a = (t % 32) <= 8 || (t % 32) >= 24;
+  const double scale = (SIGN > 0 || case_a) ? cs.x : -cs.x;
+  const double ratio = SIGN > 0 ? cs.y : -cs.y;
+  double u, v;
+  if (case_a) {
+    u = fma(-ratio, b.y, b.x);
+    v = fma(ratio, b.x, b.y);
+  } else {
+    u = fma(ratio, b.x, -b.y);
+    v = fma(ratio, b.y, b.x);
+  }
+  const double2 s = make_double2(fma(scale, u, a.x), fma(scale, v, a.y));
+  const double2 d = make_double2(fma(-scale, u, a.x), fma(-scale, v, a.y));
+  a = s;
+  b = d;
+}
+
 template <int P, int SIGN, int LEN>
 __device__ __forceinline__ void dit_stage(double2 (&x)[P]) {
   constexpr int h = LEN / 2;
 #pragma unroll
   for (int st = 0; st < P; st += LEN) {
 #pragma unroll
-    for (int j = 0; j < h; ++j) {
-      const double2 a = x[st + j];
-      const double2 b = rot64<SIGN>(x[st + j + h], j * (64 / LEN));
-      x[st + j] = cadd(a, b);
-      x[st + j + h] = csub(a, b);
-    }
+    for (int j = 0; j < h; ++j) bfly<SIGN>(x[st + j], x[st + j + h], j * (64 / LEN));
   }
 }
 
@@ -103,7 +134,7 @@ __device__ __forceinline__ void dit(double2 (&x)[P]) {
 // Column of the transpose tile holding (row k1, logical column col).
 __device__ __forceinline__ int swz(int k1, int col) { return col ^ ((k1 & 3) << 1); }
 
-// Forward transform.  In: x[m1] = z[L*m1 + l] (l = lane & (L-1)).
+// Forward transform.  In: x[bitrev(m1)] = z[L*m1 + l] (l = lane & (L-1)).
 // Out: x[s] = Z[k(l, s)], k = k1 + P*(c + P*d), k1 = l>>1, b = l&1,
 //      c = b*P/2 + s%(P/2), d = s/(P/2).
 // tw1: smem [k1][l] = e^{2 pi i l k1 / M}.  tile: smem scratch of Geo::TILE.
@@ -141,36 +172,34 @@ template <int LOGN, bool TW0, class TW>
 __device__ __forceinline__ void fft_forward_tw(double2 (&x)[Geo<LOGN>::P], double2* tile, const TW& tw, int l) {
   using G = Geo<LOGN>;
   constexpr int P = G::P, L = G::L, LOGP = G::LOGP;
-  dif<P, +1>(x);  // x[bitrev(k1)]
+  // Input in BIT-REVERSED register order: x[bitrev(m1)] = z[L*m1 + l].
+  dit<P, +1>(x);  // x[k1] natural
 #pragma unroll
-  for (int k1 = TW0 ? 0 : 1; k1 < P; ++k1) {
-    const int r = bitrev_c<LOGP>(k1);
-    x[r] = cmul(x[r], tw(k1));
-  }
+  for (int k1 = TW0 ? 0 : 1; k1 < P; ++k1) x[k1] = cmul(x[k1], tw(k1));
   __syncwarp();
 #pragma unroll
-  for (int k1 = 0; k1 < P; ++k1) tile[k1 * L + swz(k1, l)] = x[bitrev_c<LOGP>(k1)];
+  for (int k1 = 0; k1 < P; ++k1) tile[k1 * L + swz(k1, l)] = x[k1];
   __syncwarp();
   {
     const int k1 = l >> 1, b = l & 1;
 #pragma unroll
-    for (int a = 0; a < P; ++a) x[a] = tile[k1 * L + swz(k1, b + 2 * a)];
+    for (int a = 0; a < P; ++a) x[bitrev_c<LOGP>(a)] = tile[k1 * L + swz(k1, b + 2 * a)];
   }
   __syncwarp();
-  dif<P, +1>(x);  // x[bitrev(c)] = u_b[c]
+  dit<P, +1>(x);  // x[c] = u_b[c], natural
   const bool hi = (l & 1) != 0;
   double2 y[P];
 #pragma unroll
   for (int j = 0; j < P / 2; ++j) {
-    const double2 ulo = x[bitrev_c<LOGP>(j)];
-    const double2 uhi = x[bitrev_c<LOGP>(j + P / 2)];
+    const double2 ulo = x[j];
+    const double2 uhi = x[j + P / 2];
     const double2 recv = shfl_xor_c(hi ? ulo : uhi, 1);
-    const double2 u0 = hi ? recv : ulo;
-    const double2 u1 = hi ? uhi : recv;
-    // w^c with w = e^{2 pi i / 2P}, c = j + b*P/2: w^c = i^b * w^j (w^j lane-uniform)
-    const double2 t = mul_i_if(rot64<+1>(u1, (32 / P) * j), hi);
-    y[j] = cadd(u0, t);
-    y[j + P / 2] = csub(u0, t);
+    double2 u0 = hi ? recv : ulo;
+    // w^c with w = e^{2 pi i / 2P}, c = j + b*P/2: w^c = w^j * i^b (w^j lane-uniform)
+    double2 u1 = mul_i_if(hi ? uhi : recv, hi);
+    bfly<+1>(u0, u1, (32 / P) * j);
+    y[j] = u0;
+    y[j + P / 2] = u1;
   }
 #pragma unroll
   for (int s = 0; s < P; ++s) x[s] = y[s];

@@ -196,6 +196,14 @@ int upload_roots(gw_ctx* c) {
   roots[32] = make_double2(-1.0, 0.0);
   roots[48] = make_double2(0.0, -1.0);
   GW_CUDA(c, cudaMemcpyToSymbol(c_root64, roots, sizeof(roots)));
+  double2 ts[64];
+  for (int t = 0; t < 64; ++t) {
+    const long double a = 2.0L * pi * (long double)t / 64.0L;
+    const bool case_a = (t % 32) <= 8 || (t % 32) >= 24;  // |cos| >= |sin|
+    ts[t] = case_a ? make_double2((double)cosl(a), (double)(sinl(a) / cosl(a)))
+                   : make_double2((double)sinl(a), (double)(cosl(a) / sinl(a)));
+  }
+  GW_CUDA(c, cudaMemcpyToSymbol(c_ts64, ts, sizeof(ts)));
   return GW_OK;
 }
 

@@ -16,6 +16,9 @@ namespace gw {
 // e^{2 pi i t / 64}, t in [0, 64): every root of unity the in-register DFTs
 // use (sizes divide 64).  Filled from the host with correctly rounded values.
 __constant__ double2 c_root64[64];
+// Tangent-form twiddles for 6-op butterflies: for t with |cos| >= |sin|
+// (t mod 32 in [0,8] or [24,32)) (cos, tan) of 2 pi t / 64, else (sin, cot).
+__constant__ double2 c_ts64[64];
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) {
   return make_double2(a.x + b.x, a.y + b.y);
