@@ -27,10 +27,8 @@ struct TmGeo {
   static constexpr int ALLOC = (2 * COLS) <= 32 ? 32 : (2 * COLS) <= 64 ? 64 : (2 * COLS) <= 128 ? 128
                                : (2 * COLS) <= 256 ? 256 : 512;
   static_assert(2 * COLS <= 512, "two key slabs must fit the 512 TMEM columns");
-  // per-gate u32 exchange area: digit swap between the two level-warps of a
-  // component (start of a step) and the rounded lo/hi partial results of the
-  // h-pair (end of a step); the two uses never overlap in time
-  static constexpr int XCHG = 2 * 2 * G::P * 32;
+  // digit exchange between the two level-warps of one accumulator component
+  static constexpr int XCHG = LEV == 2 ? 2 * 2 * (G::P / 2) * 32 : 0;  // u32 per gate
   static size_t smem_bytes(int gc, int n) {
     const size_t lin_words = ((size_t)n + 1 + 3) & ~(size_t)3;
     return 64 /*tmem slot + mbarriers*/ + sizeof(double2) * G::TILE /*tw1'*/ +
@@ -200,23 +198,16 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
         uint32_t* to_partner = xg + (size_t)(1 - lv) * (P / 2) * 32;
         const uint32_t* from_partner = xg + (size_t)lv * (P / 2) * 32;
         uint32_t mine[P];
-        // issue all 2P shared-memory loads first (independent), then compute
-        uint32_t vr[P], va[P];
-        const uint32_t idxh = idx0 + (uint32_t)(hh * M);
-#pragma unroll
-        for (int m1 = 0; m1 < P; ++m1) {
-          const uint32_t idx = (idxh + (uint32_t)(L * m1)) & two_n_mask;
-          vr[m1] = A[idx & (N - 1)];
-          va[m1] = A[L * m1 + l + hh * M];
-        }
 #pragma unroll
         for (int m1 = 0; m1 < P; m1 += 2) {
           uint32_t oth[2];
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
-            const uint32_t idx = (idxh + (uint32_t)(L * (m1 + q))) & two_n_mask;
+            const uint32_t j = (uint32_t)(L * (m1 + q) + l + hh * M);
+            const uint32_t idx = (idx0 + (uint32_t)(L * (m1 + q)) + (uint32_t)(hh * M)) & two_n_mask;
+            const uint32_t v = A[idx & (N - 1)];
             const uint32_t neg = 0u - ((idx >> LOGN) & 1u);  // all ones past X^N
-            const uint32_t buf = ((vr[m1 + q] ^ neg) - neg) - va[m1 + q] + a.offs;
+            const uint32_t buf = ((v ^ neg) - neg) - A[j] + a.offs;
             mine[m1 + q] = (buf >> sh_mine) & base_mask;
             oth[q] = (buf >> sh_other) & base_mask;
           }
@@ -316,27 +307,15 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_tm(BrArgs a) {
         if constexpr (TWREG) fft_inverse_tw<LOGN, true>(acc, xb + (size_t)o * G::TILE, TwRegs<P>{twr}, l);
         else fft_inverse<LOGN, true>(acc, xb + (size_t)o * G::TILE, tw1, l);
       }
-      // Warp (co, 0) rounded the lo-half products, warp (co, 1) the hi half.
-      // Atomic-free update: the pair swaps half its values so that warp ho owns
-      // the coefficients j + ho*M (real / imaginary fold) and applies
-      // acc += lo + (hi << 16) with one plain read-modify-write per coefficient.
-      uint32_t* xa = xchg_all + (size_t)gl * T::XCHG + (size_t)co * 2 * P * 32;
-      uint32_t keep[P];
+      uint32_t* Ac = acc_g + co * N;
+      const int shift = 16 * ho;
 #pragma unroll
       for (int m1 = 0; m1 < P; ++m1) {
         const double2 v = m1 == 0 ? acc[0] : cmulc(acc[m1], c_root64[G::CSTEP * m1]);
-        const uint32_t rr = round_mod32(v.x), ri = round_mod32(v.y);
-        keep[m1] = ho ? ri : rr;
-        xa[(size_t)((1 - ho) * P + m1) * 32 + lane] = ho ? rr : ri;
-      }
-      named_barrier(5 + 2 * gl + co, 64);
-      if (owner && !(a.ablate & 8)) {
-        uint32_t* Ac = acc_g + co * N + ho * M;
-#pragma unroll
-        for (int m1 = 0; m1 < P; ++m1) {
-          const uint32_t recv = xa[(size_t)(ho * P + m1) * 32 + lane];
-          const uint32_t lo = ho ? recv : keep[m1], hi = ho ? keep[m1] : recv;
-          Ac[L * m1 + l] += lo + (hi << 16);
+        const uint32_t j = (uint32_t)(L * m1 + l);
+        if (owner && !(a.ablate & 8)) {
+          atomicAdd(Ac + j, round_mod32(v.x) << shift);
+          atomicAdd(Ac + j + M, round_mod32(v.y) << shift);
         }
       }
     }
