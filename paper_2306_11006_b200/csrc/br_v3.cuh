@@ -1,0 +1,390 @@
+// br_v3.cuh -- blind rotation v3: frequency-partitioned MAC, bootstrapping key
+// streamed L2 -> registers -> double-buffered TMEM.
+// Reference: gatewave/cggi.py:592-667 (`_blind_rotate_kernel`), PARAM_128 /
+// PARAM_110 geometry (N = 1024, l = 2: four gadget rows, four MAC outputs).
+//
+// CTA = GC gates x 4 warps, one CTA per SM (it owns all 512 TMEM columns).
+// Per step i, per gate:
+//   F  warp r (row r = (component r/2, level r%2)): rotate-subtract +
+//      gadget-decompose acc[r/2] (cggi.py:627-644), fold + twist, forward FFT
+//      head (DFT-16, lane twiddle, transpose, DFT-16) -> u_b[c] into U[r].
+//   M  warp w (TMEM sub-partition w) owns the frequency pairs (k1, c) with
+//      c in [4w, 4w+4): it finishes the last radix-2 stage of all four rows
+//      for its pairs, multiplies by the 16 key values of each of its 4
+//      frequencies (read from TMEM, cggi.py:648-657), and applies the first
+//      radix-2 stage of the four inverse transforms; results -> V (= U).
+//   I  warp o (output o = (component o/2, key half o%2)): inverse FFT tail,
+//      untwist, round, acc[o/2] += v << 16*(o%2) with shared-memory atomics
+//      (cggi.py:658-666; wrap-around adds commute, so the result is exact).
+// Compared to v2 (br_tmem.cuh), every shared-memory value is read once per
+// step instead of four times, and the lane-pair radix-2 stage needs no
+// shuffles or selects.  The key slab of step i+1 (128 KB: 64 complex per TMEM
+// lane) is loaded with coalesced 16-byte global loads in four groups issued at
+// the phase boundaries of step i and stored into the idle TMEM buffer with
+// tcgen05.st; it never touches shared memory (measured: staging it through
+// shared memory with cp.async.bulk + tcgen05.cp costs 256 KB of shared-memory
+// traffic per step and arrives late, profiles/r01_v3_*).
+#pragma once
+#include "blind_rotate.cuh"
+#include "mbarrier.cuh"
+#include "tmem.cuh"
+
+namespace gw {
+
+struct V3 {
+  static constexpr int LOGN = 10, LEV = 2;
+  using G = Geo<LOGN>;
+  static constexpr int N = G::N, M = G::M, P = G::P, L = G::L, R = 2 * LEV;
+  static constexpr int CIDX = 64;                   // key complexes per TMEM lane per step: 4 freqs x (4 outputs x 4 rows)
+  static constexpr int COLS = CIDX * 4;             // TMEM columns per buffer
+  static constexpr int UB = R * P * L;              // double2 per gate: U / V / transpose tiles (32 KB)
+  static constexpr int XCHG = 2 * 2 * (P / 2) * 32; // u32 per gate: digit swap between level-warps
+  static size_t smem_bytes(int gc) {
+    return (size_t)gc * (UB * sizeof(double2) + 2 * N * sizeof(uint32_t) + XCHG * sizeof(uint32_t)) +
+           (size_t)P * L * sizeof(double2) + 128;
+  }
+};
+
+// key image: [i][cidx][tmem lane] complex, cidx = q*16 + o*4 + r, tmem lane = 32*w + lane.
+// Lane (w, lane) owns frequency pairs (k1 = lane & 15, c = 4w + 2*(lane >> 4) + p), q = 2p + s,
+// s = 0: u_0 + w^c u_1, s = 1: u_0 - w^c u_1.
+__host__ __device__ __forceinline__ size_t v3_index(int i, int cidx, int tlane) {
+  return ((size_t)i * V3::CIDX + cidx) * 128 + tlane;
+}
+
+// position of lane l's pre-last-stage value u_b[c] inside the 32-wide row c of U
+__device__ __forceinline__ int v3_pos(int l) { return ((l & 1) << 4) | (l >> 1); }
+
+__device__ __forceinline__ double2 ldg_stream(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
+template <int GC>
+__global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
+  using G = V3::G;
+  constexpr int N = V3::N, M = V3::M, P = V3::P, L = V3::L, R = V3::R, LEV = V3::LEV, LOGN = V3::LOGN;
+  constexpr int UB = V3::UB, COLS = V3::COLS, CIDX = V3::CIDX;
+  // key streaming: warp (gl, w) fills cidx [gl*KPW, (gl+1)*KPW) of sub-partition w,
+  // 8 complex (32 columns, one tcgen05.st) per group, GPP groups per phase point
+  constexpr int KPW = CIDX / GC;
+  constexpr int GPP = KPW / 32;  // 4 phase points per step
+  static_assert(KPW % 32 == 0, "GC must divide 2");
+
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  double2* ubuf_all = reinterpret_cast<double2*>(smem_raw);                    // GC x [row][c][pos]
+  uint32_t* acc_all = reinterpret_cast<uint32_t*>(ubuf_all + (size_t)GC * UB);
+  uint32_t* xchg_all = acc_all + (size_t)GC * 2 * N;
+  double2* tw1 = reinterpret_cast<double2*>(xchg_all + (size_t)GC * V3::XCHG);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tw1 + P * L);
+  uint64_t* full_bar = bars;       // [2] every warp stored its share of the slab in TMEM buffer b
+  uint64_t* empty_bar = bars + 2;  // [2] every warp finished its MAC reads of buffer b
+  uint32_t* tm_slot = reinterpret_cast<uint32_t*>(bars + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, l = lane;
+  const int gl = warp >> 2, o = warp & 3;
+  const int g = blockIdx.x * GC + gl;
+  const bool active = g < a.B;
+  // inactive gate slots (last CTA) run on row 0 and discard the result, so the
+  // barrier protocol never depends on the batch size
+  const uint32_t* lin_g = a.lin + (size_t)(active ? g : 0) * a.lin_stride;
+
+  for (int t = threadIdx.x; t < P * L; t += blockDim.x) tw1[t] = a.tables[2 * G::TILE + t];
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 2; ++k) {
+      mbar_init(&full_bar[k], 4 * GC);
+      mbar_init(&empty_bar[k], 4 * GC);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tm_alloc(tm_slot, 512);
+  tm_fence_before();
+  __syncthreads();
+  tm_fence_after();
+  const uint32_t tm_base = *tm_slot;
+  const uint32_t tm_warp = tm_base + ((uint32_t)(32 * o) << 16);
+
+  // ---- key streaming (global -> registers -> TMEM) ----
+  const double2* kw_base = a.bk + (size_t)(gl * KPW) * 128 + 32 * o + lane;
+  double2 kb[GPP][8];
+  auto kissue = [&](int i, int pt) {
+    const double2* src = kw_base + (size_t)i * CIDX * 128;
+#pragma unroll
+    for (int gg = 0; gg < GPP; ++gg)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) kb[gg][k] = ldg_stream(src + (size_t)((pt * GPP + gg) * 8 + k) * 128);
+  };
+  auto kstore = [&](int buf, int pt) {
+#pragma unroll
+    for (int gg = 0; gg < GPP; ++gg)
+      tm_st32(tm_warp + (uint32_t)(buf * COLS + (gl * KPW + (pt * GPP + gg) * 8) * 4), kb[gg]);
+  };
+  auto release = [&](uint64_t* bar) {
+    tm_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar);
+  };
+  for (int pt = 0; pt < 4; ++pt) {  // prologue: slab 0 -> buffer 0
+    kissue(0, pt);
+    kstore(0, pt);
+  }
+  tm_wait_st();
+  release(&full_bar[0]);
+
+  const uint32_t two_n_mask = 2 * N - 1;
+  const uint32_t rshift = 32 - (LOGN + 1);
+  const uint32_t radd = 1u << (32 - (LOGN + 1) - 1);
+  const uint32_t base_mask = (1u << a.bg_bits) - 1;
+  const int32_t half_base = 1 << (a.bg_bits - 1);
+
+  uint32_t* acc_g = acc_all + (size_t)gl * 2 * N;
+  double2* U = ubuf_all + (size_t)gl * UB;
+  // acc <- tv * X^{-bbar} (cggi.py:612-622): warp o < 2 initialises component o
+  if (o < 2) {
+    const uint32_t bbar = ((lin_g[a.n] + radd) >> rshift) & two_n_mask;
+    const uint32_t k = (2 * N - bbar) & two_n_mask;
+    const uint32_t* tvc = a.tv + o * N;
+    for (int j = lane; j < N; j += 32) {
+      const uint32_t m = ((uint32_t)j - k) & two_n_mask;
+      acc_g[o * N + j] = m < (uint32_t)N ? tvc[m] : 0u - tvc[m - N];
+    }
+  }
+  __syncthreads();
+
+  // MAC-phase geometry of this lane: pairs (k1, c_p), p = 0, 1
+  const int mk1 = lane & 15;
+  const int mc0 = 4 * o + 2 * (lane >> 4);
+  const int pos = v3_pos(l);
+  const int bar_id = 1 + gl;
+  const TwSmem tws{tw1, L, l};
+
+  const bool prof = a.prof != nullptr && blockIdx.x == 0 && gl == 0 && lane == 0;
+  long long pt_[6] = {0, 0, 0, 0, 0, 0};
+  long long tprev = clock64();
+  auto mark = [&](int ph) {
+    if (prof) {
+      const long long t = clock64();
+      pt_[ph] += t - tprev;
+      tprev = t;
+    }
+  };
+
+  uint32_t a_next = __ldg(lin_g);
+  for (int i = 0; i < a.n; ++i) {
+    const int cur = i & 1, nxt = cur ^ 1;
+    const bool pre = i + 1 < a.n;
+    const uint32_t a_i = a_next;
+    if (pre) {
+      a_next = __ldg(lin_g + i + 1);
+      kissue(i + 1, 0);
+    }
+    // ---------------- F: row r = o ----------------
+    {
+      const int cr = o / LEV, lv = o % LEV;
+      const uint32_t* A = acc_g + cr * N;
+      const uint32_t abar = ((a_i + radd) >> rshift) & two_n_mask;
+      const uint32_t idx0 = ((uint32_t)l - abar) & two_n_mask;
+      double2 x[P];
+      // The two level-warps of component cr split the coefficients by half
+      // (warp lv takes j + lv*M), extract BOTH digit levels of their half and
+      // swap the other level's digits through shared memory.
+      const int hh = lv;
+      const int sh_mine = 32 - (lv + 1) * a.bg_bits, sh_other = 32 - (2 - lv) * a.bg_bits;
+      uint32_t* xg = xchg_all + (size_t)gl * V3::XCHG + (size_t)cr * 2 * (P / 2) * 32;
+      uint32_t* to_partner = xg + (size_t)(1 - lv) * (P / 2) * 32;
+      const uint32_t* from_partner = xg + (size_t)lv * (P / 2) * 32;
+      uint32_t mine[P];
+      const uint32_t idxh = idx0 + (uint32_t)(hh * M);
+#pragma unroll
+      for (int m1 = 0; m1 < P; m1 += 2) {
+        uint32_t oth[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const uint32_t idx = (idxh + (uint32_t)(L * (m1 + q))) & two_n_mask;
+          const uint32_t v = A[idx & (N - 1)];
+          const uint32_t neg = 0u - ((idx >> LOGN) & 1u);  // all ones past X^N
+          const uint32_t buf = ((v ^ neg) - neg) - A[L * (m1 + q) + l + hh * M] + a.offs;
+          mine[m1 + q] = (buf >> sh_mine) & base_mask;
+          oth[q] = (buf >> sh_other) & base_mask;
+        }
+        to_partner[(m1 / 2) * 32 + lane] = oth[0] | (oth[1] << 16);
+      }
+      named_barrier(5 + 2 * gl + cr, 64);
+#pragma unroll
+      for (int m1 = 0; m1 < P; m1 += 2) {
+        const uint32_t w = from_partner[(m1 / 2) * 32 + lane];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const uint32_t rv = q ? (w >> 16) : (w & 0xFFFFu);
+          const uint32_t re = hh ? rv : mine[m1 + q], im = hh ? mine[m1 + q] : rv;
+          double2 v = make_double2(digit_to_double(re, half_base), digit_to_double(im, half_base));
+          if (m1 + q > 0) v = cmul(v, c_root64[G::CSTEP * (m1 + q)]);
+          x[bitrev_c<G::LOGP>(m1 + q)] = v;  // DIT forward takes bit-reversed input
+        }
+      }
+      double2* tile = U + (size_t)o * P * L;
+      fft_forward_head<LOGN, true>(x, tile, tws, l);
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < P; ++c) tile[c * L + pos] = x[c];
+    }
+    mark(0);
+    if (pre) {  // buffer nxt is free once every warp finished MAC(i-1)
+      if (i >= 1) mbar_wait(&empty_bar[nxt], (uint32_t)(((i - 1) >> 1) & 1));
+      tm_fence_after();
+      kstore(nxt, 0);
+      kissue(i + 1, 1);
+    }
+    named_barrier(bar_id, 128);  // U complete
+    mark(1);
+    // ---------------- M: frequency pairs (mk1, mc0 + p) of all rows ----------------
+    mbar_wait(&full_bar[cur], (uint32_t)((i >> 1) & 1));
+    tm_fence_after();
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const int c = mc0 + p;
+      const double2 tw = c_root64[2 * c];  // e^{2 pi i c / 32}
+      double2 D[R][2];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double2* row = U + ((size_t)r * P + c) * L;
+        const double2 u0 = row[mk1], u1 = row[16 + mk1];
+        const double2 t = cmul(u1, tw);
+        D[r][0] = cadd(u0, t);
+        D[r][1] = csub(u0, t);
+      }
+      double2 O[4][2];  // [output][s]
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        uint32_t kw[2][32];
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf)
+          tm_ld_raw<32>(tm_warp + (uint32_t)(cur * COLS + ((2 * p + s) * 16 + hf * 8) * 4), kw[hf]);
+        tm_wait_ld();
+#pragma unroll
+        for (int oo = 0; oo < 4; ++oo)
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const uint32_t* k4 = kw[oo >> 1] + ((oo & 1) * 4 + r) * 4;
+            const double2 kr = make_double2(__hiloint2double(k4[1], k4[0]), __hiloint2double(k4[3], k4[2]));
+            O[oo][s] = r == 0 ? cmul(D[r][s], kr) : cfma(O[oo][s], D[r][s], kr);
+          }
+      }
+#pragma unroll
+      for (int oo = 0; oo < 4; ++oo) {
+        double2* row = U + ((size_t)oo * P + c) * L;
+        row[mk1] = cadd(O[oo][0], O[oo][1]);
+        row[16 + mk1] = cmulc(csub(O[oo][0], O[oo][1]), tw);
+      }
+    }
+    release(&empty_bar[cur]);
+    mark(2);
+    if (pre) {
+      kstore(nxt, 1);
+      kissue(i + 1, 2);
+    }
+    named_barrier(bar_id, 128);  // V complete
+    mark(3);
+    // ---------------- I: output o = (component o/2, half o%2) ----------------
+    {
+      double2 x[P];
+      double2* tile = U + (size_t)o * P * L;
+#pragma unroll
+      for (int c = 0; c < P; ++c) x[bitrev_c<G::LOGP>(c)] = tile[c * L + pos];
+      fft_inverse_tail<LOGN, true>(x, tile, tws, l);
+      if (pre) {
+        kstore(nxt, 2);
+        kissue(i + 1, 3);
+      }
+      if (active) {
+        uint32_t* Ac = acc_g + (o >> 1) * N;
+        const int shift = 16 * (o & 1);
+#pragma unroll
+        for (int m1 = 0; m1 < P; ++m1) {
+          const double2 v = m1 == 0 ? x[0] : cmulc(x[m1], c_root64[G::CSTEP * m1]);
+          const uint32_t j = (uint32_t)(L * m1 + l);
+          atomicAdd(Ac + j, round_mod32(v.x) << shift);
+          atomicAdd(Ac + j + M, round_mod32(v.y) << shift);
+        }
+      }
+    }
+    mark(4);
+    if (pre) {
+      kstore(nxt, 3);
+      tm_wait_st();
+      release(&full_bar[nxt]);
+    }
+    named_barrier(bar_id, 128);  // acc updated before the next decomposition
+    mark(5);
+  }
+  if (prof)
+    for (int ph = 0; ph < 6; ++ph) a.prof[o * 6 + ph] = pt_[ph];
+  if (active && o < 2) {
+    uint32_t* dst = a.acc_out + ((size_t)g * 2 + o) * N;
+    for (int j = lane; j < N; j += 32) dst[j] = acc_g[o * N + j];
+  }
+  tm_fence_before();
+  __syncthreads();
+  if (warp == 0) tm_dealloc(tm_base, 512);
+}
+
+// Key image for v3 (reference: cggi.py:283-285 keeps the NTT-domain copy).  One
+// warp per (i, r, c, h) polynomial: balanced 16-bit split, fold + twist, the
+// same forward head as the gate kernel, then the last radix-2 stage for every
+// (k1, c) pair, scaled by 1/M and scattered to [i][cidx][tmem lane].
+__global__ void __launch_bounds__(128) k_bk_to_v3(const uint32_t* __restrict__ bk_coeff, int n,
+                                                  const double2* __restrict__ tables, double2* __restrict__ img) {
+  using G = V3::G;
+  constexpr int N = V3::N, M = V3::M, P = V3::P, L = V3::L, R = V3::R;
+  __shared__ double2 tw1[P * L];
+  __shared__ double2 tiles[4][P * L];
+  for (int t = threadIdx.x; t < P * L; t += blockDim.x) tw1[t] = tables[2 * G::TILE + t];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, l = lane;
+  const long long job = (long long)blockIdx.x * 4 + warp;  // ((i*R + r)*2 + c)*2 + h
+  if (job >= (long long)n * R * 4) return;
+  const int h = (int)(job & 1), c = (int)((job >> 1) & 1);
+  const int r = (int)((job >> 2) % R);
+  const int i = (int)((job >> 2) / R);
+  const uint32_t* poly = bk_coeff + (((size_t)i * R + r) * 2 + c) * N;
+  double2 x[P];
+#pragma unroll
+  for (int m1 = 0; m1 < P; ++m1) {
+    int32_t part[2];
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int32_t w = (int32_t)poly[L * m1 + l + hh * M];
+      const int32_t lo = (int32_t)(int16_t)(w & 0xFFFF);
+      part[hh] = h == 0 ? lo : (int32_t)(((int64_t)w - lo) >> 16);
+    }
+    double2 v = make_double2((double)part[0], (double)part[1]);
+    if (m1 > 0) v = cmul(v, c_root64[G::CSTEP * m1]);
+    x[bitrev_c<G::LOGP>(m1)] = v;
+  }
+  double2* tile = tiles[warp];
+  fft_forward_head<V3::LOGN, true>(x, tile, TwSmem{tw1, L, l}, l);
+  __syncwarp();
+#pragma unroll
+  for (int cc = 0; cc < P; ++cc) tile[cc * L + v3_pos(l)] = x[cc];
+  __syncwarp();
+  const double scale = 1.0 / (double)M;
+  const int oo = c * 2 + h;
+  const int k1 = lane & 15;
+#pragma unroll
+  for (int w = 0; w < 4; ++w)
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const int cf = 4 * w + 2 * (lane >> 4) + p;
+      const double2 u0 = tile[cf * L + k1], u1 = tile[cf * L + 16 + k1];
+      const double2 t = cmul(u1, c_root64[2 * cf]);
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const double2 d = s ? csub(u0, t) : cadd(u0, t);
+        const int cidx = (2 * p + s) * 16 + oo * 4 + r;
+        img[v3_index(i, cidx, 32 * w + lane)] = make_double2(d.x * scale, d.y * scale);
+      }
+    }
+}
+
+}  // namespace gw

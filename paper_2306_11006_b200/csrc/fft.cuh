@@ -241,4 +241,56 @@ __device__ __forceinline__ void fft_inverse_tw(double2 (&x)[Geo<LOGN>::P], doubl
   dit<P, -1>(x);  // x[m1]
 }
 
+// ---- split transforms for the frequency-partitioned MAC (br_v3.cuh) --------
+// The radix-2 stage across lane pairs (F3 above) is not done in registers:
+// the forward "head" stops after F2 with x[c] = u_b[c] (lane l = 2*k1 + b),
+// and the MAC phase, which gathers the values of all rows through shared
+// memory anyway, applies  D(+/-) = u_0[c] +/- w^c u_1[c]  (w = e^{2 pi i/2P})
+// for the (k1, c) pairs it owns.  The inverse "tail" starts from
+// u[bitrev(c)] = u_b[c] (b = 0: O+ + O-, b = 1: (O+ - O-) conj(w^c)).
+// No shuffles and no lane-parity selects remain in the transforms.
+template <int LOGN, bool TW0, class TW>
+__device__ __forceinline__ void fft_forward_head(double2 (&x)[Geo<LOGN>::P], double2* tile, const TW& tw, int l) {
+  using G = Geo<LOGN>;
+  constexpr int P = G::P, L = G::L, LOGP = G::LOGP;
+  dit<P, +1>(x);
+#pragma unroll
+  for (int k1 = TW0 ? 0 : 1; k1 < P; ++k1) x[k1] = cmul(x[k1], tw(k1));
+  __syncwarp();
+#pragma unroll
+  for (int k1 = 0; k1 < P; ++k1) tile[k1 * L + swz(k1, l)] = x[k1];
+  __syncwarp();
+  {
+    const int k1 = l >> 1, b = l & 1;
+#pragma unroll
+    for (int a = 0; a < P; ++a) x[bitrev_c<LOGP>(a)] = tile[k1 * L + swz(k1, b + 2 * a)];
+  }
+  __syncwarp();
+  dit<P, +1>(x);  // x[c] = u_b[c]
+}
+
+// In: x[bitrev(c)] = u_b[c].  Out: x[m1] = M * z[L*m1 + l] (in place).
+template <int LOGN, bool TW0, class TW>
+__device__ __forceinline__ void fft_inverse_tail(double2 (&x)[Geo<LOGN>::P], double2* tile, const TW& tw, int l) {
+  using G = Geo<LOGN>;
+  constexpr int P = G::P, L = G::L, LOGP = G::LOGP;
+  dit<P, -1>(x);  // x[a]
+  __syncwarp();
+  {
+    const int k1 = l >> 1, b = l & 1;
+#pragma unroll
+    for (int a = 0; a < P; ++a) tile[k1 * L + swz(k1, b + 2 * a)] = x[a];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k1 = 0; k1 < P; ++k1) x[bitrev_c<LOGP>(k1)] = tile[k1 * L + swz(k1, l)];
+  __syncwarp();
+#pragma unroll
+  for (int k1 = TW0 ? 0 : 1; k1 < P; ++k1) {
+    const int r = bitrev_c<LOGP>(k1);
+    x[r] = cmulc(x[r], tw(k1));
+  }
+  dit<P, -1>(x);  // x[m1]
+}
+
 }  // namespace gw

@@ -17,6 +17,7 @@
 #include "../../include/gatewave_b200.h"
 #include "blind_rotate.cuh"
 #include "br_tmem.cuh"
+#include "br_v3.cuh"
 #include "gates.cuh"
 #include "keyswitch.cuh"
 #include "ks_tc.cuh"
@@ -46,6 +47,7 @@ struct gw_ctx {
   // keys
   double2* bk_fft = nullptr;
   size_t bk_fft_count = 0;
+  double2* bk_v3 = nullptr;    // v3 key image (br_v3.cuh), N = 1024 and l = 2 only
   uint32_t* ksk = nullptr;
   uint8_t* kimg = nullptr;     // keyswitch key as INT8 tensor-core B image (ks_tc.cuh)
   int kt_ntiles = 0, kt_kblocks = 0;
@@ -81,7 +83,9 @@ struct gw_ctx {
   int64_t launches = 0;
   long long* br_prof = nullptr;  // device buffer for phase cycle counters (GATEWAVE_BR_PROFILE=1)
   int br_ablate = 0;              // GATEWAVE_BR_ABLATE (debug timing only; results become wrong)
-  int br_variant = 1;  // 1: TMEM 4-warp kernel where it fits, 0: 2-warp kernel (GATEWAVE_BR_KERNEL=v1)
+  // 2: v3 (frequency-partitioned MAC, TMA + tcgen05.cp key) where it applies (N = 1024, l = 2),
+  // 1: v2 TMEM 4-warp kernel, 0: v1 2-warp kernel (GATEWAVE_BR_KERNEL=v3|v2|v1)
+  int br_variant = 2;
   std::string err;
 };
 
@@ -258,8 +262,28 @@ int launch_tm(gw_ctx* c, const BrArgs& a) {
   return rc;
 }
 
+template <int GC>
+int launch_v3_g(gw_ctx* c, const BrArgs& a0) {
+  BrArgs a = a0;
+  a.bk = c->bk_v3;
+  const size_t smem = V3::smem_bytes(GC);
+  GW_CUDA(c, cudaFuncSetAttribute(k_blind_rotate_v3<GC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  a.gates_per_cta = GC;
+  const int grid = (a.B + GC - 1) / GC;
+  k_blind_rotate_v3<GC><<<grid, 128 * GC, smem, c->stream>>>(a);
+  GW_LAUNCHED(c);
+  return GW_OK;
+}
+
+// v3: one CTA per SM; two gates per CTA once the batch exceeds one per SM.
+int launch_v3(gw_ctx* c, const BrArgs& a) {
+  if (a.B > c->sm_count) return launch_v3_g<2>(c, a);
+  return launch_v3_g<1>(c, a);
+}
+
 template <int LOGN>
 int launch_br_n(gw_ctx* c, const BrArgs& a) {
+  if (LOGN == 10 && c->p.l == 2 && c->br_variant == 2 && c->bk_v3) return launch_v3(c, a);
   switch (c->p.l) {
     case 1: return c->br_variant ? launch_tm<LOGN, 1>(c, a) : launch_br_t<LOGN, 1>(c, a);
     case 2: return c->br_variant ? launch_tm<LOGN, 2>(c, a) : launch_br_t<LOGN, 2>(c, a);
@@ -560,7 +584,8 @@ int gw_create(int device, gw_ctx** out) {
   if (!rc) cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
   if (!rc && (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess)) rc = GW_ERR_CUDA;
   if (!rc) rc = upload_roots(c);
-  if (const char* v = getenv("GATEWAVE_BR_KERNEL")) c->br_variant = strcmp(v, "v1") == 0 ? 0 : 1;
+  if (const char* v = getenv("GATEWAVE_BR_KERNEL"))
+    c->br_variant = strcmp(v, "v1") == 0 ? 0 : strcmp(v, "v2") == 0 ? 1 : 2;
   if (const char* v = getenv("GATEWAVE_KS_KERNEL")) c->ks_variant = strcmp(v, "cuda") == 0 ? 0 : 1;
   if (const char* v = getenv("GATEWAVE_BR_ABLATE")) c->br_ablate = atoi(v);
   if (const char* v = getenv("GATEWAVE_BR_PROFILE"))
@@ -579,6 +604,7 @@ int gw_destroy(gw_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   cudaFree(c->bk_fft);
+  cudaFree(c->bk_v3);
   cudaFree(c->ksk);
   cudaFree(c->kimg);
   cudaFree(c->ks_ut);
@@ -704,6 +730,19 @@ int gw_upload_keys(gw_ctx* c, const uint32_t* bk_coeff, const uint32_t* ksk) {
       c->bk_fft_count = nfft;
     }
     int rc = launch_bk(c, bk_dev);
+    cudaFree(c->bk_v3);
+    c->bk_v3 = nullptr;
+    if (rc == GW_OK && c->logn == 10 && l == 2) {
+      const size_t cnt = (size_t)n * V3::CIDX * 128;
+      e = cudaMalloc(&c->bk_v3, cnt * sizeof(double2));
+      if (e == cudaSuccess) {
+        const long long jobs = (long long)n * 2 * l * 4;
+        k_bk_to_v3<<<(unsigned)((jobs + 3) / 4), 128, 0, c->stream>>>(bk_dev, n, c->tables, c->bk_v3);
+        e = cudaGetLastError();
+        if (e == cudaSuccess) c->launches++;
+      }
+      if (e != cudaSuccess) rc = fail(c, GW_ERR_CUDA, std::string("v3 key image: ") + cudaGetErrorString(e));
+    }
     cudaError_t es = cudaStreamSynchronize(c->stream);
     cudaFree(bk_dev);
     if (rc) return rc;

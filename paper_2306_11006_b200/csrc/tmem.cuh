@@ -37,6 +37,26 @@ __device__ __forceinline__ void tm_st4(uint32_t taddr, double2 v) {
                : "memory");
 }
 
+// 32 lanes x 32 consecutive columns: eight complex doubles per lane.
+__device__ __forceinline__ void tm_st32(uint32_t taddr, const double2 (&v)[8]) {
+  uint32_t r[32];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    r[4 * k] = __double2loint(v[k].x);
+    r[4 * k + 1] = __double2hiint(v[k].x);
+    r[4 * k + 2] = __double2loint(v[k].y);
+    r[4 * k + 3] = __double2hiint(v[k].y);
+  }
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
 // Raw 32-bit loads of NC consecutive columns, no wait (caller batches tm_wait_ld).
 template <int NC>
 __device__ __forceinline__ void tm_ld_raw(uint32_t taddr, uint32_t (&r)[NC]) {
