@@ -19,13 +19,16 @@
 // Compared to v2 (br_tmem.cuh), every shared-memory value is read once per
 // step instead of four times, and the lane-pair radix-2 stage needs no
 // shuffles or selects.  The key slab of step i+1 (128 KB: 64 complex per TMEM
-// lane) is loaded with coalesced 16-byte global loads in four groups issued at
-// the phase boundaries of step i and stored into the idle TMEM buffer with
-// tcgen05.st; it never touches shared memory (measured: staging it through
-// shared memory with cp.async.bulk + tcgen05.cp costs 256 KB of shared-memory
-// traffic per step and arrives late, profiles/r01_v3_*).
+// lane) goes into the idle TMEM buffer either by the warps themselves (LDG
+// mode, GC >= 2: coalesced 16-byte loads issued at the phase boundaries of
+// step i, tcgen05.st) or, where 128 KB of shared memory is spare (GC = 1), by
+// one thread: cp.async.bulk L2 -> shared memory, tcgen05.cp -> TMEM.
+// Staging through shared memory costs 256 KB of shared-memory traffic per SM
+// and step, which the GC >= 2 configurations cannot afford (measured,
+// DESIGN.md §4).
 #pragma once
 #include "blind_rotate.cuh"
+#include "ks_tc.cuh"
 #include "mbarrier.cuh"
 #include "tmem.cuh"
 
@@ -39,8 +42,11 @@ struct V3 {
   static constexpr int COLS = CIDX * 4;             // TMEM columns per buffer
   static constexpr int UB = R * P * L;              // double2 per gate: U / V / transpose tiles (32 KB)
   static constexpr int XCHG = 2 * 2 * (P / 2) * 32; // u32 per gate: digit swap between level-warps
-  static size_t smem_bytes(int gc) {
-    return (size_t)gc * (UB * sizeof(double2) + 2 * N * sizeof(uint32_t) + XCHG * sizeof(uint32_t)) +
+  static constexpr int SLAB = CIDX * 128 * 16;      // key bytes per step (128 KB)
+  // TMA mode stages the slab in shared memory (only where it fits: GC = 1)
+  static size_t smem_bytes(int gc, bool tma) {
+    return (tma ? (size_t)SLAB : 0) +
+           (size_t)gc * (UB * sizeof(double2) + 2 * N * sizeof(uint32_t) + XCHG * sizeof(uint32_t)) +
            (size_t)P * L * sizeof(double2) + 128;
   }
 };
@@ -61,26 +67,39 @@ __device__ __forceinline__ double2 ldg_stream(const double2* p) {
   return v;
 }
 
-template <int GC>
+__device__ __forceinline__ void tm_cp_128x256b(uint32_t taddr, uint64_t desc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(desc) : "memory");
+}
+
+// Key streaming modes.  LDG (GC >= 2): every warp loads its share of the next
+// slab with 16-byte global loads at the four phase points of a step and stores
+// it into the idle TMEM buffer (tcgen05.st.32x32b.x4 straight from the load
+// registers).  TMA (GC = 1, where 128 KB of shared memory is spare): warp 0
+// copies the slab L2 -> shared memory (cp.async.bulk) -> TMEM (tcgen05.cp),
+// so no compute warp spends registers or issue slots on the key.
+template <int GC, bool TMA>
 __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
   using G = V3::G;
   constexpr int N = V3::N, M = V3::M, P = V3::P, L = V3::L, R = V3::R, LEV = V3::LEV, LOGN = V3::LOGN;
   constexpr int UB = V3::UB, COLS = V3::COLS, CIDX = V3::CIDX;
   // key streaming: warp (gl, w) fills cidx [gl*KPW, (gl+1)*KPW) of sub-partition w,
   // 8 complex (32 columns, one tcgen05.st) per group, GPP groups per phase point
-  constexpr int KPW = CIDX / GC;
-  constexpr int GPP = KPW / 32;  // 4 phase points per step
-  static_assert(KPW % 32 == 0, "GC must divide 2");
+  // LDG mode: the slab is 8 groups of 8 cidx; warp (gl, w) owns groups gl, gl+GC, ...
+  // and handles group list entry j at phase point j % 4 (GC = 1: two per point)
+  constexpr int NG = (8 + GC - 1) / GC;     // max groups per warp
+  constexpr int GPP = (NG + 3) / 4;         // groups per phase point
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  double2* ubuf_all = reinterpret_cast<double2*>(smem_raw);                    // GC x [row][c][pos]
+  unsigned char* stage = smem_raw;                                               // TMA mode: 128 KB slab
+  double2* ubuf_all = reinterpret_cast<double2*>(smem_raw + (TMA ? V3::SLAB : 0));  // GC x [row][c][pos]
   uint32_t* acc_all = reinterpret_cast<uint32_t*>(ubuf_all + (size_t)GC * UB);
   uint32_t* xchg_all = acc_all + (size_t)GC * 2 * N;
   double2* tw1 = reinterpret_cast<double2*>(xchg_all + (size_t)GC * V3::XCHG);
   uint64_t* bars = reinterpret_cast<uint64_t*>(tw1 + P * L);
   uint64_t* full_bar = bars;       // [2] every warp stored its share of the slab in TMEM buffer b
   uint64_t* empty_bar = bars + 2;  // [2] every warp finished its MAC reads of buffer b
-  uint32_t* tm_slot = reinterpret_cast<uint32_t*>(bars + 4);
+  uint64_t* stage_bar = bars + 4;  // TMA mode: slab landed in shared memory
+  uint32_t* tm_slot = reinterpret_cast<uint32_t*>(bars + 6);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, l = lane;
   const int gl = warp >> 2, o = warp & 3;
@@ -93,9 +112,10 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
   for (int t = threadIdx.x; t < P * L; t += blockDim.x) tw1[t] = a.tables[2 * G::TILE + t];
   if (threadIdx.x == 0) {
     for (int k = 0; k < 2; ++k) {
-      mbar_init(&full_bar[k], 4 * GC);
+      mbar_init(&full_bar[k], TMA ? 1 : 4 * GC);
       mbar_init(&empty_bar[k], 4 * GC);
     }
+    mbar_init(stage_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) tm_alloc(tm_slot, 512);
@@ -105,32 +125,62 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
   const uint32_t tm_base = *tm_slot;
   const uint32_t tm_warp = tm_base + ((uint32_t)(32 * o) << 16);
 
-  // ---- key streaming (global -> registers -> TMEM) ----
-  const double2* kw_base = a.bk + (size_t)(gl * KPW) * 128 + 32 * o + lane;
+  // ---- key streaming ----
+  const double2* kw_base = a.bk + (size_t)32 * o + lane;
   double2 kb[GPP][8];
+  // LDG mode, phase point pt of step i: load / store this warp's groups
   auto kissue = [&](int i, int pt) {
-    const double2* src = kw_base + (size_t)i * CIDX * 128;
+    if constexpr (!TMA) {
+      const double2* src = kw_base + (size_t)i * CIDX * 128;
 #pragma unroll
-    for (int gg = 0; gg < GPP; ++gg)
+      for (int gg = 0; gg < GPP; ++gg) {
+        const int j = pt * GPP + gg, grp = gl + GC * j;
+        if (j < NG && grp < 8)
 #pragma unroll
-      for (int k = 0; k < 8; ++k) kb[gg][k] = ldg_stream(src + (size_t)((pt * GPP + gg) * 8 + k) * 128);
+          for (int k = 0; k < 8; ++k) kb[gg][k] = ldg_stream(src + (size_t)(grp * 8 + k) * 128);
+      }
+    }
   };
   auto kstore = [&](int buf, int pt) {
+    if constexpr (!TMA) {
 #pragma unroll
-    for (int gg = 0; gg < GPP; ++gg)
-      tm_st32(tm_warp + (uint32_t)(buf * COLS + (gl * KPW + (pt * GPP + gg) * 8) * 4), kb[gg]);
+      for (int gg = 0; gg < GPP; ++gg) {
+        const int j = pt * GPP + gg, grp = gl + GC * j;
+        if (j < NG && grp < 8)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) tm_st4(tm_warp + (uint32_t)(buf * COLS + (grp * 8 + k) * 4), kb[gg][k]);
+      }
+    }
   };
   auto release = [&](uint64_t* bar) {
     tm_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(bar);
   };
-  for (int pt = 0; pt < 4; ++pt) {  // prologue: slab 0 -> buffer 0
-    kissue(0, pt);
-    kstore(0, pt);
+  // TMA mode: slab -> TMEM buffer, 32 copies of 128 lanes x 8 columns (two cidx each)
+  const uint32_t stage_s = smem_u32(stage);
+  const unsigned char* img = reinterpret_cast<const unsigned char*>(a.bk);
+  auto copy_to_tmem = [&](int buf) {
+#pragma unroll 4
+    for (int j = 0; j < COLS / 8; ++j)
+      tm_cp_128x256b(tm_base + (uint32_t)(buf * COLS + 8 * j), umma_desc(stage_s + j * 4096, 2048, 128));
+    umma_commit(&full_bar[buf]);
+  };
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {  // prologue: slab 0 -> buffer 0
+      mbar_expect_tx(stage_bar, V3::SLAB);
+      bulk_g2s(stage, img, V3::SLAB, stage_bar);
+      mbar_wait(stage_bar, 0);
+      copy_to_tmem(0);
+    }
+  } else {
+    for (int pt = 0; pt < 4; ++pt) {  // prologue: slab 0 -> buffer 0
+      kissue(0, pt);
+      kstore(0, pt);
+    }
+    tm_wait_st();
+    release(&full_bar[0]);
   }
-  tm_wait_st();
-  release(&full_bar[0]);
 
   const uint32_t two_n_mask = 2 * N - 1;
   const uint32_t rshift = 32 - (LOGN + 1);
@@ -230,7 +280,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
       for (int c = 0; c < P; ++c) tile[c * L + pos] = x[c];
     }
     mark(0);
-    if (pre) {  // buffer nxt is free once every warp finished MAC(i-1)
+    if (!TMA && pre) {  // buffer nxt is free once every warp finished MAC(i-1)
       if (i >= 1) mbar_wait(&empty_bar[nxt], (uint32_t)(((i - 1) >> 1) & 1));
       tm_fence_after();
       kstore(nxt, 0);
@@ -241,6 +291,10 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
     // ---------------- M: frequency pairs (mk1, mc0 + p) of all rows ----------------
     mbar_wait(&full_bar[cur], (uint32_t)((i >> 1) & 1));
     tm_fence_after();
+    if (TMA && threadIdx.x == 0 && pre) {  // the copies of slab i are done: refill the staging buffer
+      mbar_expect_tx(stage_bar, V3::SLAB);
+      bulk_g2s(stage, img + (size_t)(i + 1) * V3::SLAB, V3::SLAB, stage_bar);
+    }
 #pragma unroll
     for (int p = 0; p < 2; ++p) {
       const int c = mc0 + p;
@@ -310,10 +364,19 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
       }
     }
     mark(4);
-    if (pre) {
+    if (!TMA && pre) {
       kstore(nxt, 3);
       tm_wait_st();
       release(&full_bar[nxt]);
+    }
+    // TMA mode, slab i+1: staging -> TMEM buffer nxt.  The whole of warp 0
+    // waits (the bar.sync below is warp-aligned), one thread issues.
+    if (TMA && warp == 0 && pre) {
+      mbar_wait(stage_bar, (uint32_t)((i + 1) & 1));
+      if (i >= 1) mbar_wait(&empty_bar[nxt], (uint32_t)(((i - 1) >> 1) & 1));
+      tm_fence_after();
+      if (threadIdx.x == 0) copy_to_tmem(nxt);
+      __syncwarp();
     }
     named_barrier(bar_id, 128);  // acc updated before the next decomposition
     mark(5);
