@@ -58,8 +58,12 @@ __host__ __device__ __forceinline__ size_t v3_index(int i, int cidx, int tlane) 
   return ((size_t)i * V3::CIDX + cidx) * 128 + tlane;
 }
 
-// position of lane l's pre-last-stage value u_b[c] inside the 32-wide row c of U
-__device__ __forceinline__ int v3_pos(int l) { return ((l & 1) << 4) | (l >> 1); }
+// Slot of u_b[c] for k1 inside the 32-wide row c of U: 16 b + (k1 ^ 4b).  Both
+// access patterns are conflict-free 16-byte accesses: a quarter-warp of the
+// row warps (k1 in 4q..4q+3, b = 0, 1) and of the MAC warps (8 consecutive
+// k1, fixed b) each touch 8 distinct bank groups.
+__device__ __forceinline__ int v3_slot(int k1, int b) { return (b << 4) | (k1 ^ (b << 2)); }
+__device__ __forceinline__ int v3_pos(int l) { return v3_slot(l >> 1, l & 1); }
 
 __device__ __forceinline__ double2 ldg_stream(const double2* p) {
   double2 v;
@@ -303,7 +307,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const double2* row = U + ((size_t)r * P + c) * L;
-        const double2 u0 = row[mk1], u1 = row[16 + mk1];
+        const double2 u0 = row[v3_slot(mk1, 0)], u1 = row[v3_slot(mk1, 1)];
         const double2 t = cmul(u1, tw);
         D[r][0] = cadd(u0, t);
         D[r][1] = csub(u0, t);
@@ -328,8 +332,8 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
 #pragma unroll
       for (int oo = 0; oo < 4; ++oo) {
         double2* row = U + ((size_t)oo * P + c) * L;
-        row[mk1] = cadd(O[oo][0], O[oo][1]);
-        row[16 + mk1] = cmulc(csub(O[oo][0], O[oo][1]), tw);
+        row[v3_slot(mk1, 0)] = cadd(O[oo][0], O[oo][1]);
+        row[v3_slot(mk1, 1)] = cmulc(csub(O[oo][0], O[oo][1]), tw);
       }
     }
     release(&empty_bar[cur]);
@@ -439,7 +443,7 @@ __global__ void __launch_bounds__(128) k_bk_to_v3(const uint32_t* __restrict__ b
 #pragma unroll
     for (int p = 0; p < 2; ++p) {
       const int cf = 4 * w + 2 * (lane >> 4) + p;
-      const double2 u0 = tile[cf * L + k1], u1 = tile[cf * L + 16 + k1];
+      const double2 u0 = tile[cf * L + v3_slot(k1, 0)], u1 = tile[cf * L + v3_slot(k1, 1)];
       const double2 t = cmul(u1, c_root64[2 * cf]);
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
