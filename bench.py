@@ -345,9 +345,22 @@ def run_ours(args):
     flops_per_bootstrap = 249_856 * P.n                      # SURVEY.md §8(d), FP64 path
     achieved = flops_per_bootstrap * br_items / (br_ms / 1e3) / 1e12 if br_ms > 0 else 0.0
     bk_bytes = P.n * 2 * (2 * P.l) * 2 * (P.N // 2) * 16    # FFT-domain key, one pass
+    # the kernel the engine launches for this batch (gw_api.cu launch_v3: gates per CTA =
+    # ceil(G / SMs), one CTA per SM; TMA key staging only at one gate per CTA)
+    gc = min(4, max(1, -(-G // torch.cuda.get_device_properties(local).multi_processor_count)))
+    kname = f"k_blind_rotate_v3<{gc},{1 if gc == 1 else 0}>"
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+            t = json.load(f).get(kname)
+        if t and t["gates"] == G:
+            traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
+    except (OSError, ValueError, KeyError):
+        pass
     roofline = {"bound": "fp64", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
-                "kernel": "k_blind_rotate<10,2>",
+                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                "traffic_unit": "bytes per launch (ncu dram read+write, profiles/r01_ncu_traffic.json)",
+                "kernel": kname,
                 "per_launch_ms": br_ms / launches_br,
                 "work_per_launch": f"{G} bootstraps x {flops_per_bootstrap} FLOP",
                 "kernel_share_of_step": br_ms / max(sum(step_ms), 1e-9),
