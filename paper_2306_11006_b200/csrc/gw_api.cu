@@ -6,6 +6,7 @@
 //   k_lin -> k_blind_rotate -> k_zero_units -> k_keyswitch -> k_cheap
 // All launches go to the context stream; only the host-pointer entry points
 // synchronise (they must hand results back to the caller).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -92,7 +93,8 @@ struct gw_ctx {
 
 struct gw_plan {
   int64_t n_levels = 0;
-  std::vector<int> J, U, C;            // per level counts
+  std::vector<int> J, U, C;            // per segment counts
+  std::vector<int64_t> seg_first;      // (n_levels + 1): first segment of each level
   std::vector<size_t> job_off, unit_off, cheap_off;
   LinJob* jobs = nullptr;
   KsUnit* units = nullptr;
@@ -1072,12 +1074,20 @@ int gw_plan_create(gw_ctx* c, int64_t n_levels, const int64_t* offs, const int32
   std::vector<LinJob> jobs;
   std::vector<KsUnit> units;
   std::vector<CheapUnit> cheap;
+  // Every level is cut into segments of at most kSegGates gates (the gates of
+  // a level are independent): a segment is one launch set, so scratch memory
+  // stays bounded (~1 GB) however wide the level is.  kSegGates is a multiple
+  // of 148 SMs x 4 gates per CTA, i.e. whole waves of the blind rotation.
+  constexpr int64_t kSegGates = 148 * 4 * 28;
   for (int64_t lv = 0; lv < n_levels; ++lv) {
+   p->seg_first.push_back((int64_t)p->J.size());
+   for (int64_t s0 = offs[lv]; s0 < offs[lv + 1] || s0 == offs[lv]; s0 += kSegGates) {
+    const int64_t s1 = std::min<int64_t>(offs[lv + 1], s0 + kSegGates);
     const size_t j0 = jobs.size(), u0 = units.size(), c0 = cheap.size();
     p->job_off.push_back(j0);
     p->unit_off.push_back(u0);
     p->cheap_off.push_back(c0);
-    for (int64_t g = offs[lv]; g < offs[lv + 1]; ++g) {
+    for (int64_t g = s0; g < s1; ++g) {
       const int op = opcodes[g];
       const int ar = arity_of(op);
       if (ar < 0) {
@@ -1105,7 +1115,10 @@ int gw_plan_create(gw_ctx* c, int64_t n_levels, const int64_t* offs, const int32
     p->U.push_back((int)(units.size() - u0));
     p->C.push_back((int)(cheap.size() - c0));
     if (p->J.back() > p->max_jobs) p->max_jobs = p->J.back();
+    if (s1 >= offs[lv + 1]) break;
+   }
   }
+  p->seg_first.push_back((int64_t)p->J.size());
   cudaError_t e = cudaSuccess;
   if (!jobs.empty()) e = cudaMalloc(&p->jobs, jobs.size() * sizeof(LinJob));
   if (e == cudaSuccess && !units.empty()) e = cudaMalloc(&p->units, units.size() * sizeof(KsUnit));
@@ -1131,10 +1144,11 @@ int gw_plan_run_levels(gw_ctx* c, gw_plan* p, int64_t first, int64_t last) {
   if (!c->wires) return fail(c, GW_ERR_STATE, "wire store not allocated");
   if (first < 0) first = 0;
   if (last > p->n_levels) last = p->n_levels;
+  if (first >= last) return GW_OK;
   cudaSetDevice(c->device);
-  for (int64_t lv = first; lv < last; ++lv) {
-    rc = run_level(c, c->wires, c->Wp, c->wires, c->Wp, p->jobs + p->job_off[lv], p->J[lv],
-                   p->units + p->unit_off[lv], p->U[lv], p->cheap + p->cheap_off[lv], p->C[lv]);
+  for (int64_t sg = p->seg_first[first]; sg < p->seg_first[last]; ++sg) {
+    rc = run_level(c, c->wires, c->Wp, c->wires, c->Wp, p->jobs + p->job_off[sg], p->J[sg],
+                   p->units + p->unit_off[sg], p->U[sg], p->cheap + p->cheap_off[sg], p->C[sg]);
     if (rc) return rc;
   }
   return GW_OK;

@@ -43,25 +43,40 @@ def owners(c: Circuit, schedule: Schedule, world: int) -> dict[int, int]:
 
 
 def exchange_plan(c: Circuit, schedule: Schedule, world: int) -> ExchangePlan:
-    own = owners(c, schedule, world)
-    by_id = {g.id: g for g in c.gates}
-    needed_by: dict[int, set] = {}
-    for g in c.gates:
-        for w in g.operands:
-            if w in own:
-                needed_by.setdefault(w, set()).add(own[g.id])
-    out_wires = {w for p in c.outputs for w in p.wires}
+    """Per level and rank, the produced wires that another rank reads later or
+    that are circuit outputs.  Vectorised over the circuit arrays (numpy)."""
+    from .runtime import _circuit_arrays
+    ids, _, opnd, _ = _circuit_arrays(c)
+    nb = [(wi, b) for wi, wave in enumerate(schedule.waves) for b in wave]
+    sizes = np.fromiter((len(b.gate_ids) for _, b in nb), dtype=np.int64, count=len(nb))
+    total = int(sizes.sum())
+    gid = np.fromiter((g for _, b in nb for g in b.gate_ids), dtype=np.int64, count=total)
+    wave = np.repeat(np.fromiter((wi for wi, _ in nb), dtype=np.int64, count=len(nb)), sizes)
+    rank = np.repeat(np.fromiter((b.worker % world for _, b in nb), dtype=np.int64, count=len(nb)), sizes)
+    top = int(max(c.max_wire, ids.max() if len(ids) else 0)) + 1
+    own = np.full(top, -1, dtype=np.int64)
+    own[gid] = rank
+    send = np.zeros(top, dtype=bool)
+    # reader rank of every operand slot (circuit order) vs the writer's rank
+    reader = own[ids]
+    valid = opnd >= 0
+    w = np.where(valid, opnd, 0)
+    cross = valid & (own[w] >= 0) & (own[w] != reader[:, None])
+    send[w[cross]] = True
+    for p in c.outputs:
+        send[np.asarray(p.wires, np.int64)] = True
+    keep = send[gid]
     sends, pad = [], []
-    for wave in schedule.waves:
-        per_rank = [[] for _ in range(world)]
-        for b in wave:
-            for gid in b.gate_ids:
-                r = own[gid]
-                if gid in out_wires or (needed_by.get(gid, set()) - {r}):
-                    per_rank[r].append(gid)
-        sends.append([np.asarray(x, np.int64) for x in per_rank])
-        pad.append(max(len(x) for x in per_rank))
-    del by_id
+    levels = len(schedule.waves)
+    order = np.lexsort((rank[keep], wave[keep]))
+    kg, kw, kr = gid[keep][order], wave[keep][order], rank[keep][order]
+    # split into [level][rank] (schedule order inside each bucket)
+    key = kw * world + kr
+    bounds = np.searchsorted(key, np.arange(levels * world + 1))
+    for L in range(levels):
+        per_rank = [kg[bounds[L * world + r]:bounds[L * world + r + 1]] for r in range(world)]
+        sends.append(per_rank)
+        pad.append(max((len(x) for x in per_rank), default=0))
     return ExchangePlan(world=world, sends=sends, pad=pad)
 
 
@@ -119,7 +134,8 @@ def evaluate_distributed(c: Circuit, schedule: Schedule, mats: dict, ek: EvalKey
     import torch.distributed as dist
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     p = ek.params
-    plan = compile_plan(c, schedule, worker=rank, world=world)
+    from .runtime import _cached_plan
+    plan = _cached_plan(c, schedule, worker=rank, world=world)
     xplan = exchange_plan(c, schedule, world)
     slots = c.max_wire + 1
     if levels_factory is None:

@@ -126,6 +126,27 @@ class LevelPlan:
     gates: int
 
 
+def _circuit_arrays(c: Circuit):
+    """(ids, opcode codes, operands (G, 3) -1 padded, arity) in circuit order,
+    cached on the circuit (one pass over the Gate objects)."""
+    cached = c.__dict__.get("_plan_arrays")
+    if cached is not None:
+        return cached
+    G = len(c.gates)
+    ids = np.fromiter((g.id for g in c.gates), dtype=np.int64, count=G)
+    kinds = [as_kind(g.opcode) for g in c.gates]
+    codes = np.fromiter((_OPC[k.value] for k in kinds), dtype=np.int32, count=G)
+    ar = np.fromiter((len(g.operands) for g in c.gates), dtype=np.int32, count=G)
+    flat = np.fromiter((w for g in c.gates for w in (*g.operands, -1, -1, -1)[:3]), dtype=np.int64, count=3 * G)
+    out = (ids, codes, flat.reshape(G, 3), ar)
+    c.__dict__["_plan_arrays"] = out
+    return out
+
+
+_ARITY_OF_CODE = np.array([GATE_ARITY[as_kind(k)] for k in _OPC], dtype=np.int32)
+_BOOTS_OF_CODE = np.array([BOOTSTRAPS_PER_GATE[as_kind(k)] for k in _OPC], dtype=np.int64)
+
+
 def compile_plan(c: Circuit, schedule: Schedule, worker: int | None = None,
                  world: int | None = None) -> LevelPlan:
     """Flatten a schedule into level arrays.  worker=None merges every worker's
@@ -134,46 +155,66 @@ def compile_plan(c: Circuit, schedule: Schedule, worker: int | None = None,
 
     Static SSA check over the whole schedule (the reference's per-access
     WireStore guards, runtime.py:83-96): every wire is written once, and read
-    only in a wave strictly after the one that writes it.
+    only in a wave strictly after the one that writes it.  Vectorised (numpy)
+    so that 10^7-gate netlists compile in seconds.
     """
-    by_id = {g.id: g for g in c.gates}
-    scheduled = [gid for wave in schedule.waves for b in wave for gid in b.gate_ids]
-    if sorted(scheduled) != sorted(by_id):
+    ids, codes, opnd, ar = _circuit_arrays(c)
+    nb = [(wi, b) for wi, wave in enumerate(schedule.waves) for b in wave]
+    sizes = np.fromiter((len(b.gate_ids) for _, b in nb), dtype=np.int64, count=len(nb))
+    total = int(sizes.sum())
+    gid = np.fromiter((g for _, b in nb for g in b.gate_ids), dtype=np.int64, count=total)
+    wave = np.repeat(np.fromiter((wi for wi, _ in nb), dtype=np.int64, count=len(nb)), sizes)
+    bcode = np.repeat(np.fromiter((_OPC[as_kind(b.opcode).value] for _, b in nb), dtype=np.int32,
+                                  count=len(nb)), sizes)
+    if total != len(ids) or not np.array_equal(np.sort(gid), np.sort(ids)):
         raise EvaluateError("schedule does not cover this circuit's gates")
-    written_at: dict[int, int] = {w: -1 for w in c.input_wires}
-    for wi, wave in enumerate(schedule.waves):
-        for b in wave:
-            for gid in b.gate_ids:
-                for w in by_id[gid].operands:
-                    if written_at.get(w, wi) >= wi:
-                        raise EvaluateError(f"wire {w} read before it was written")
-        for b in wave:
-            for gid in b.gate_ids:
-                if gid in written_at:
-                    raise EvaluateError(f"wire {gid} written twice")
-                written_at[gid] = wi
-    offs, codes, opnd, outs = [0], [], [], []
-    boots = 0
-    for wave in schedule.waves:
-        for b in wave:
-            if worker is not None and (b.worker % world if world else b.worker) != worker:
-                continue
-            kind = as_kind(b.opcode)
-            ar = GATE_ARITY[kind]
-            boots += BOOTSTRAPS_PER_GATE[kind] * len(b.gate_ids)
-            for gid in b.gate_ids:
-                g = by_id[gid]
-                if as_kind(g.opcode) is not kind or len(g.operands) != ar:
-                    raise EvaluateError(f"gate {gid} does not match its batch opcode")
-                codes.append(_OPC[kind.value])
-                ops = list(g.operands) + [-1] * (3 - ar)
-                opnd.append(ops)
-                outs.append(gid)
-        offs.append(len(codes))
-    return LevelPlan(level_offsets=np.asarray(offs, np.int64),
-                     opcodes=np.asarray(codes, np.int32),
-                     operands=np.asarray(opnd, np.int32).reshape(-1, 3),
-                     out_ids=np.asarray(outs, np.int32), bootstraps=boots, gates=len(codes))
+    top = int(max(c.max_wire, ids.max() if len(ids) else 0, opnd.max() if opnd.size else 0)) + 1
+    pos_of = np.full(top, -1, dtype=np.int64)
+    pos_of[ids] = np.arange(len(ids))
+    pos = pos_of[gid]                                   # circuit position of every scheduled gate
+    # written once: the coverage check above plus unique circuit ids
+    if len(np.unique(ids)) != len(ids):
+        raise EvaluateError("a wire is written twice")
+    written_at = np.full(top, np.iinfo(np.int64).max, dtype=np.int64)
+    written_at[np.fromiter(c.input_wires, dtype=np.int64, count=len(c.input_wires))] = -1
+    if len(c.input_wires) and np.isin(ids, np.fromiter(c.input_wires, dtype=np.int64)).any():
+        raise EvaluateError("a gate writes a circuit input wire")
+    written_at[gid] = wave
+    ops = opnd[pos]                                     # (total, 3)
+    valid = ops >= 0
+    ok = np.where(valid, written_at[np.where(valid, ops, 0)] < wave[:, None], True)
+    if not ok.all():
+        k = int(np.argwhere(~ok)[0][0])
+        raise EvaluateError(f"wire {int(ops[k][np.argmax(~ok[k])])} read before it was written")
+    if (codes[pos] != bcode).any() or (ar[pos] != _ARITY_OF_CODE[bcode]).any():
+        k = int(np.argmax((codes[pos] != bcode) | (ar[pos] != _ARITY_OF_CODE[bcode])))
+        raise EvaluateError(f"gate {int(gid[k])} does not match its batch opcode")
+    if worker is not None:
+        bw = np.repeat(np.fromiter((b.worker for _, b in nb), dtype=np.int64, count=len(nb)), sizes)
+        keep = (bw % world if world else bw) == worker
+        gid, wave, bcode, ops = gid[keep], wave[keep], bcode[keep], ops[keep]
+    offs = np.zeros(len(schedule.waves) + 1, dtype=np.int64)
+    np.add.at(offs, wave + 1, 1)
+    offs = np.cumsum(offs)
+    return LevelPlan(level_offsets=offs, opcodes=bcode.astype(np.int32),
+                     operands=ops.astype(np.int32).reshape(-1, 3),
+                     out_ids=gid.astype(np.int32), bootstraps=int(_BOOTS_OF_CODE[bcode].sum()),
+                     gates=len(gid))
+
+
+def _cached_plan(c: Circuit, schedule: Schedule, worker: int | None = None,
+                 world: int | None = None) -> LevelPlan:
+    """compile_plan, memoised on the circuit per (schedule, worker, world): the
+    static checks and the flattening are one-time host work, like the
+    reference's schedule construction."""
+    cache = c.__dict__.setdefault("_plan_cache", {})
+    key = (id(schedule), worker, world)
+    hit = cache.get(key)
+    if hit is not None and hit[0] is schedule:
+        return hit[1]
+    plan = compile_plan(c, schedule, worker=worker, world=world)
+    cache[key] = (schedule, plan)
+    return plan
 
 
 def evaluate(c: Circuit, schedule: Schedule, inputs: Mapping[str, np.ndarray], keys,
@@ -194,7 +235,7 @@ def evaluate(c: Circuit, schedule: Schedule, inputs: Mapping[str, np.ndarray], k
         from .exchange import evaluate_distributed
         return evaluate_distributed(c, schedule, mats, ek, group=group)
 
-    plan = compile_plan(c, schedule, worker=None)
+    plan = _cached_plan(c, schedule)
     eng = ek.engine()
     eng.wires_alloc(c.max_wire + 1)
     for port in c.inputs:
