@@ -59,6 +59,57 @@ __global__ void k(const uint32_t* img, int* bad, int lbo, int sbo) {
   if (warp == 0) tm_dealloc(base, 512);
 }
 
+// throughput of the v3 TMA-mode key path: (a) 32 x tcgen05.cp.128x256b of a
+// resident 128 KB slab, (b) cp.async.bulk of 128 KB, (c) both chained
+__global__ void k_rate(const unsigned char* img, long long* out, int iters) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 131072);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(smem + 131072 + 32);
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tm_alloc(slot, 512);
+  tm_fence_before();
+  __syncthreads();
+  tm_fence_after();
+  const uint32_t base = *slot;
+  if (threadIdx.x == 0) {
+    const uint32_t s0 = smem_u32(smem);
+    uint32_t ph0 = 0, ph1 = 0;
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      for (int j = 0; j < 32; ++j) tm_cp(base + 8 * j, umma_desc(s0 + j * 4096, 2048, 128));
+      umma_commit(&bar[1]);
+      mbar_wait(&bar[1], ph1); ph1 ^= 1;
+    }
+    long long t1 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      mbar_expect_tx(&bar[0], 131072);
+      bulk_g2s(smem, img + (size_t)(it % 64) * 131072, 131072, &bar[0]);
+      mbar_wait(&bar[0], ph0); ph0 ^= 1;
+    }
+    long long t2 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      mbar_expect_tx(&bar[0], 131072);
+      bulk_g2s(smem, img + (size_t)(it % 64) * 131072, 131072, &bar[0]);
+      mbar_wait(&bar[0], ph0); ph0 ^= 1;
+      for (int j = 0; j < 32; ++j) tm_cp(base + 256 * (it & 1) + 8 * j, umma_desc(s0 + j * 4096, 2048, 128));
+      umma_commit(&bar[1]);
+      mbar_wait(&bar[1], ph1); ph1 ^= 1;
+    }
+    long long t3 = clock64();
+    out[blockIdx.x * 3 + 0] = (t1 - t0) / iters;
+    out[blockIdx.x * 3 + 1] = (t2 - t1) / iters;
+    out[blockIdx.x * 3 + 2] = (t3 - t2) / iters;
+  }
+  tm_fence_before();
+  __syncthreads();
+  if (warp == 0) tm_dealloc(base, 512);
+}
+
 int main() {
   uint32_t* h = new uint32_t[32768];
   for (int cidx = 0; cidx < 64; ++cidx)
@@ -70,7 +121,7 @@ int main() {
   cudaMalloc(&bad, 4);
   cudaMemcpy(d, h, 131072, cudaMemcpyHostToDevice);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072 + 64);
-  int combos[2][2] = {{2048, 128}, {128, 2048}};
+  int combos[1][2] = {{2048, 128}};
   for (auto& cb : combos) {
     cudaMemset(bad, 0, 4);
     k<<<1, 128, 131072 + 64>>>(d, bad, cb[0], cb[1]);
@@ -78,6 +129,22 @@ int main() {
     int hb = -1;
     cudaMemcpy(&hb, bad, 4, cudaMemcpyDeviceToHost);
     printf("lbo=%d sbo=%d: %s, mismatches %d\n", cb[0], cb[1], cudaGetErrorString(e), hb);
+  }
+  {
+    unsigned char* img;
+    long long* o;
+    cudaMalloc(&img, (size_t)64 * 131072);
+    cudaMemset(img, 3, (size_t)64 * 131072);
+    cudaMalloc(&o, 148 * 3 * 8);
+    cudaFuncSetAttribute(k_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072 + 64);
+    for (int grid : {1, 148}) {
+      k_rate<<<grid, 128, 131072 + 64>>>(img, o, 200);
+      cudaError_t e = cudaDeviceSynchronize();
+      long long h[3];
+      cudaMemcpy(h, o, sizeof(h), cudaMemcpyDeviceToHost);
+      printf("grid %3d (%s): tcgen05.cp 128 KB %lld cyc, bulk 128 KB %lld cyc, bulk+cp %lld cyc\n", grid,
+             cudaGetErrorString(e), h[0], h[1], h[2]);
+    }
   }
   return 0;
 }
