@@ -387,8 +387,9 @@ def run_ours(args):
     parity["e2e_matches_device"] = bool(np.array_equal(r, res))
 
     # ---- config 2 app latency: adder8 + 8-bit multiplier through evaluate() --
+    # BASELINE configs[1] is a one-GPU latency workload: measured at N = 1 only
     netlist = None
-    if not args.no_netlist:
+    if not args.no_netlist and ws == 1:
         netlist = config2_latency(ks, P, eng)
 
     # ---- CPU baseline (oracle port), rank 0 at N=1 only --------------------
