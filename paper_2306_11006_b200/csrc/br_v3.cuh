@@ -39,7 +39,10 @@ struct V3 {
   using G = Geo<LOGN>;
   static constexpr int N = G::N, M = G::M, P = G::P, L = G::L, R = 2 * LEV;
   static constexpr int CIDX = 64;                   // key complexes per TMEM lane per step: 4 freqs x (4 outputs x 4 rows)
-  static constexpr int COLS = CIDX * 4;             // TMEM columns per buffer
+  static constexpr int COLS = CIDX * 4;             // TMEM columns per step slab
+  // TMEM: a ring of 7 key chunks (chunk = the 16 key values of one of a lane's
+  // 4 frequencies = 64 columns) + the lane-twiddle table (16 complex = 64 columns)
+  static constexpr int RING = 7, CHUNK = 64, TWCOL = RING * CHUNK;
   static constexpr int UB = R * P * L;              // double2 per gate: U / V / transpose tiles (32 KB)
   static constexpr int XCHG = 2 * 2 * (P / 2) * 32; // u32 per gate: digit swap between level-warps
   static constexpr int SLAB = CIDX * 128 * 16;      // key bytes per step (128 KB)
@@ -47,7 +50,7 @@ struct V3 {
   static size_t smem_bytes(int gc, bool tma) {
     return (tma ? (size_t)SLAB : 0) +
            (size_t)gc * (UB * sizeof(double2) + 2 * N * sizeof(uint32_t) + XCHG * sizeof(uint32_t)) +
-           (size_t)P * L * sizeof(double2) + 128;
+           (gc >= 4 ? (size_t)P * L * sizeof(double2) : 0) + 128;
   }
 };
 
@@ -57,6 +60,21 @@ struct V3 {
 __host__ __device__ __forceinline__ size_t v3_index(int i, int cidx, int tlane) {
   return ((size_t)i * V3::CIDX + cidx) * 128 + tlane;
 }
+
+// Lane twiddles streamed from TMEM eight at a time (register-lean variant for
+// GC >= 3): the transforms call tw(k1) for k1 = 0..15 in order.
+struct TwTmemHalves {
+  uint32_t taddr;
+  mutable uint32_t r[32];
+  __device__ __forceinline__ double2 operator()(int k1) const {
+    if ((k1 & 7) == 0) {
+      tm_ld_raw<32>(taddr + (uint32_t)((k1 >> 3) * 32), r);
+      tm_wait_ld();
+    }
+    const uint32_t* w = r + (k1 & 7) * 4;
+    return make_double2(__hiloint2double(w[1], w[0]), __hiloint2double(w[3], w[2]));
+  }
+};
 
 // Slot of u_b[c] for k1 inside the 32-wide row c of U: 16 b + (k1 ^ 4b).  Both
 // access patterns are conflict-free 16-byte accesses: a quarter-warp of the
@@ -102,8 +120,12 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
   double2* ubuf_all = reinterpret_cast<double2*>(smem_raw + (TMA ? V3::SLAB : 0));  // GC x [row][c][pos]
   uint32_t* acc_all = reinterpret_cast<uint32_t*>(ubuf_all + (size_t)GC * UB);
   uint32_t* xchg_all = acc_all + (size_t)GC * 2 * N;
+  // GC = 4 (128 registers): lane twiddles from a shared-memory table; otherwise TMEM
+  constexpr bool kTwSmem = GC >= 4;
   double2* tw1 = reinterpret_cast<double2*>(xchg_all + (size_t)GC * V3::XCHG);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(tw1 + P * L);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tw1 + (kTwSmem ? P * L : 0));
+  if constexpr (kTwSmem)
+    for (int t = threadIdx.x; t < P * L; t += blockDim.x) tw1[t] = a.tables[2 * G::TILE + t];
   uint64_t* full_bar = bars;       // [2] every warp stored its share of the slab in TMEM buffer b
   uint64_t* empty_bar = bars + 2;  // [2] every warp finished its MAC reads of buffer b
   uint64_t* stage_bar = bars + 4;  // TMA mode: slab landed in shared memory
@@ -117,7 +139,6 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
   // barrier protocol never depends on the batch size
   const uint32_t* lin_g = a.lin + (size_t)(active ? g : 0) * a.lin_stride;
 
-  for (int t = threadIdx.x; t < P * L; t += blockDim.x) tw1[t] = a.tables[2 * G::TILE + t];
   if (threadIdx.x == 0) {
     for (int k = 0; k < 2; ++k) {
       mbar_init(&full_bar[k], TMA ? 1 : 4 * GC);
@@ -132,6 +153,22 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
   tm_fence_after();
   const uint32_t tm_base = *tm_slot;
   const uint32_t tm_warp = tm_base + ((uint32_t)(32 * o) << 16);
+  const uint32_t tm_tw = tm_warp + (uint32_t)V3::TWCOL;
+  // lane twiddles tw'[k1][l] -> TMEM columns TWCOL + 4 k1 of every sub-partition
+  // (read with tcgen05.ld in the transforms instead of 32 LDS.128 per warp-step)
+  if (!kTwSmem && gl == 0) {
+#pragma unroll
+    for (int k1 = 0; k1 < P; ++k1) tm_st4(tm_tw + (uint32_t)(4 * k1), __ldg(a.tables + 2 * G::TILE + k1 * L + l));
+    tm_wait_st();
+  }
+  // key chunk q of step i: ring slot (4 i + q) mod 7 when the twiddles live in
+  // TMEM; plain double buffering (slot 4 (i & 1) + q) when they do not (GC = 4:
+  // the ring's chunk-3 reuse couples the gates of a CTA one step tighter)
+  constexpr bool kRing = !kTwSmem;
+  auto kcol = [&](int slot_i, int q) -> uint32_t {
+    const int sl = slot_i + q;
+    return (uint32_t)((kRing && sl >= V3::RING ? sl - V3::RING : sl) * V3::CHUNK);
+  };
 
   // ---- key streaming ----
   const double2* kw_base = a.bk + (size_t)32 * o + lane;
@@ -149,14 +186,22 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
       }
     }
   };
-  auto kstore = [&](int buf, int pt) {
+  // store for step i+1 (ring base slot sn); its chunk 3 reuses the slot of step i's
+  // chunk 0, so it waits until every warp has finished MAC(i) (empty barrier of step i)
+  auto kstore = [&](int i, int sn, int pt) {
     if constexpr (!TMA) {
 #pragma unroll
       for (int gg = 0; gg < GPP; ++gg) {
         const int j = pt * GPP + gg, grp = gl + GC * j;
-        if (j < NG && grp < 8)
+        if (j < NG && grp < 8) {
+          if (kRing && grp >> 1 == 3) {
+            mbar_wait(&empty_bar[i & 1], (uint32_t)((i >> 1) & 1));
+            tm_fence_after();
+          }
 #pragma unroll
-          for (int k = 0; k < 8; ++k) tm_st4(tm_warp + (uint32_t)(buf * COLS + (grp * 8 + k) * 4), kb[gg][k]);
+          for (int k = 0; k < 8; ++k)
+            tm_st4(tm_warp + kcol(sn, grp >> 1) + (uint32_t)(((grp & 1) * 8 + k) * 4), kb[gg][k]);
+        }
       }
     }
   };
@@ -168,10 +213,11 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
   // TMA mode: slab -> TMEM buffer, 32 copies of 128 lanes x 8 columns (two cidx each)
   const uint32_t stage_s = smem_u32(stage);
   const unsigned char* img = reinterpret_cast<const unsigned char*>(a.bk);
-  auto copy_to_tmem = [&](int buf) {
+  auto copy_to_tmem = [&](int buf, int sn) {
 #pragma unroll 4
-    for (int j = 0; j < COLS / 8; ++j)
-      tm_cp_128x256b(tm_base + (uint32_t)(buf * COLS + 8 * j), umma_desc(stage_s + j * 4096, 2048, 128));
+    for (int j = 0; j < COLS / 8; ++j)  // 8-column block j holds cidx 2j, 2j+1 (chunk j / 8)
+      tm_cp_128x256b(tm_base + kcol(sn, j >> 3) + (uint32_t)((j & 7) * 8),
+                     umma_desc(stage_s + j * 4096, 2048, 128));
     umma_commit(&full_bar[buf]);
   };
   if constexpr (TMA) {
@@ -179,12 +225,19 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
       mbar_expect_tx(stage_bar, V3::SLAB);
       bulk_g2s(stage, img, V3::SLAB, stage_bar);
       mbar_wait(stage_bar, 0);
-      copy_to_tmem(0);
+      copy_to_tmem(0, 0);
     }
   } else {
-    for (int pt = 0; pt < 4; ++pt) {  // prologue: slab 0 -> buffer 0
+    for (int pt = 0; pt < 4; ++pt) {  // prologue: slab 0 -> ring slots 0..3 (no chunk-3 wait)
       kissue(0, pt);
-      kstore(0, pt);
+#pragma unroll
+      for (int gg = 0; gg < GPP; ++gg) {
+        const int j = pt * GPP + gg, grp = gl + GC * j;
+        if (j < NG && grp < 8)
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            tm_st4(tm_warp + kcol(0, grp >> 1) + (uint32_t)(((grp & 1) * 8 + k) * 4), kb[gg][k]);
+      }
     }
     tm_wait_st();
     release(&full_bar[0]);
@@ -215,7 +268,19 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
   const int mc0 = 4 * o + 2 * (lane >> 4);
   const int pos = v3_pos(l);
   const int bar_id = 1 + gl;
-  const TwSmem tws{tw1, L, l};
+  // lane twiddles for one transform, from TMEM into registers
+  auto load_tw = [&](double2 (&tw)[P]) {
+    uint32_t r[2][32];
+    tm_ld_raw<32>(tm_tw, r[0]);
+    tm_ld_raw<32>(tm_tw + 32, r[1]);
+    tm_wait_ld();
+#pragma unroll
+    for (int k1 = 0; k1 < P; ++k1) {
+      const uint32_t* w = r[k1 >> 3] + (k1 & 7) * 4;
+      tw[k1] = make_double2(__hiloint2double(w[1], w[0]), __hiloint2double(w[3], w[2]));
+    }
+  };
+  int sc = 0;  // ring slot base of step i: (4 i) mod 7
 
   const bool prof = a.prof != nullptr && blockIdx.x == 0 && gl == 0 && lane == 0;
   long long pt_[6] = {0, 0, 0, 0, 0, 0};
@@ -231,6 +296,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
   uint32_t a_next = __ldg(lin_g);
   for (int i = 0; i < a.n; ++i) {
     const int cur = i & 1, nxt = cur ^ 1;
+    const int sn = kRing ? (sc + 4 >= V3::RING ? sc + 4 - V3::RING : sc + 4) : 4 - sc;  // slot base of step i+1
     const bool pre = i + 1 < a.n;
     const uint32_t a_i = a_next;
     if (pre) {
@@ -308,7 +374,15 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
         }
       }
       double2* tile = U + (size_t)o * P * L;
-      fft_forward_head<LOGN, true>(x, tile, tws, l);
+      if constexpr (GC <= 2) {
+        double2 tw[P];
+        load_tw(tw);
+        fft_forward_head<LOGN, true>(x, tile, TwRegs<P>{tw}, l);
+      } else if constexpr (!kTwSmem) {
+        fft_forward_head<LOGN, true>(x, tile, TwTmemHalves{tm_tw}, l);
+      } else {
+        fft_forward_head<LOGN, true>(x, tile, TwSmem{tw1, L, l}, l);
+      }
       __syncwarp();
 #pragma unroll
       for (int c = 0; c < P; ++c) tile[c * L + pos] = x[c];
@@ -317,7 +391,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
     if (!TMA && pre) {  // buffer nxt is free once every warp finished MAC(i-1)
       if (i >= 1) mbar_wait(&empty_bar[nxt], (uint32_t)(((i - 1) >> 1) & 1));
       tm_fence_after();
-      kstore(nxt, 0);
+      kstore(i, sn, 0);
       kissue(i + 1, 1);
     }
     named_barrier(bar_id, 128);  // U complete
@@ -348,7 +422,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
         uint32_t kw[2][32];
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf)
-          tm_ld_raw<32>(tm_warp + (uint32_t)(cur * COLS + ((2 * p + s) * 16 + hf * 8) * 4), kw[hf]);
+          tm_ld_raw<32>(tm_warp + kcol(sc, 2 * p + s) + (uint32_t)(hf * 32), kw[hf]);
         tm_wait_ld();
 #pragma unroll
         for (int oo = 0; oo < 4; ++oo)
@@ -369,7 +443,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
     release(&empty_bar[cur]);
     mark(2);
     if (pre) {
-      kstore(nxt, 1);
+      kstore(i, sn, 1);
       kissue(i + 1, 2);
     }
     named_barrier(bar_id, 128);  // V complete
@@ -380,9 +454,17 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
       double2* tile = U + (size_t)o * P * L;
 #pragma unroll
       for (int c = 0; c < P; ++c) x[bitrev_c<G::LOGP>(c)] = tile[c * L + pos];
-      fft_inverse_tail<LOGN, true>(x, tile, tws, l);
+      if constexpr (GC <= 2) {
+        double2 tw[P];
+        load_tw(tw);
+        fft_inverse_tail<LOGN, true>(x, tile, TwRegs<P>{tw}, l);
+      } else if constexpr (!kTwSmem) {
+        fft_inverse_tail<LOGN, true>(x, tile, TwTmemHalves{tm_tw}, l);
+      } else {
+        fft_inverse_tail<LOGN, true>(x, tile, TwSmem{tw1, L, l}, l);
+      }
       if (pre) {
-        kstore(nxt, 2);
+        kstore(i, sn, 2);
         kissue(i + 1, 3);
       }
       if (active) {
@@ -399,7 +481,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
     }
     mark(4);
     if (!TMA && pre) {
-      kstore(nxt, 3);
+      kstore(i, sn, 3);
       tm_wait_st();
       release(&full_bar[nxt]);
     }
@@ -408,12 +490,14 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
     if (TMA && warp == 0 && pre) {
       mbar_wait(stage_bar, (uint32_t)((i + 1) & 1));
       if (i >= 1) mbar_wait(&empty_bar[nxt], (uint32_t)(((i - 1) >> 1) & 1));
+      mbar_wait(&empty_bar[cur], (uint32_t)((i >> 1) & 1));  // chunk 3 reuses step i's chunk-0 slot
       tm_fence_after();
-      if (threadIdx.x == 0) copy_to_tmem(nxt);
+      if (threadIdx.x == 0) copy_to_tmem(nxt, sn);
       __syncwarp();
     }
     named_barrier(bar_id, 128);  // acc updated before the next decomposition
     mark(5);
+    sc = sn;
   }
   if (prof)
     for (int ph = 0; ph < 6; ++ph) a.prof[o * 6 + ph] = pt_[ph];
