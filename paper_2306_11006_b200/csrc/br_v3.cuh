@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
   const uint32_t radd = 1u << (32 - (LOGN + 1) - 1);
   const uint32_t base_mask = (1u << a.bg_bits) - 1;
   const int32_t half_base = 1 << (a.bg_bits - 1);
+  const double dmagic = 6755399441055744.0 + (double)half_base;
 
   uint32_t* acc_g = acc_all + (size_t)gl * 2 * N;
   double2* U = ubuf_all + (size_t)gl * UB;
@@ -343,7 +344,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
           for (int q = 0; q < 2; ++q) {
             const uint32_t rv = q ? (w >> 16) : (w & 0xFFFFu);
             const uint32_t re = hh ? rv : mine[m1 + q], im = hh ? mine[m1 + q] : rv;
-            double2 v = make_double2(digit_to_double(re, half_base), digit_to_double(im, half_base));
+            double2 v = make_double2(digit_to_double_lo(re, dmagic), digit_to_double_lo(im, dmagic));
             if (m1 + q > 0) v = cmul(v, c_root64[G::CSTEP * (m1 + q)]);
             x[bitrev_c<G::LOGP>(m1 + q)] = v;  // DIT forward takes bit-reversed input
           }
@@ -366,7 +367,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
             const uint32_t idx = (idx0 + (uint32_t)(L * m1 + hh * M)) & two_n_mask;
             const uint32_t neg = 0u - ((idx >> LOGN) & 1u);  // all ones past X^N
             const uint32_t buf = ((vr[2 * m1 + hh] ^ neg) - neg) - va[2 * m1 + hh] + a.offs;
-            dd[hh] = digit_to_double((buf >> sh) & base_mask, half_base);
+            dd[hh] = digit_to_double_lo((buf >> sh) & base_mask, dmagic);
           }
           double2 v = make_double2(dd[0], dd[1]);
           if (m1 > 0) v = cmul(v, c_root64[G::CSTEP * m1]);

@@ -52,6 +52,11 @@ __device__ __forceinline__ double small_int_to_double(int32_t d) {
 __device__ __forceinline__ double digit_to_double(uint32_t u, int32_t half) {
   return __longlong_as_double((long long)(0x4338000000000000LL - half) + (long long)u) - 6755399441055744.0;
 }
+// Same value without 64-bit integer arithmetic: hi word 0x43380000, lo word u
+// is exactly 1.5*2^52 + u; subtracting the (exact) constant 1.5*2^52 + half.
+__device__ __forceinline__ double digit_to_double_lo(uint32_t u, double magic_plus_half) {
+  return __hiloint2double(0x43380000, (int)u) - magic_plus_half;
+}
 // x * i^b for a lane-dependent bit b (integer sign flip + selects, no FP op).
 __device__ __forceinline__ double2 mul_i_if(double2 t, bool b) {
   const double nty = __longlong_as_double(__double_as_longlong(t.y) ^ (long long)0x8000000000000000ULL);
