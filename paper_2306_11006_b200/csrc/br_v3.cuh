@@ -32,6 +32,10 @@
 #include "mbarrier.cuh"
 #include "tmem.cuh"
 
+#ifndef GW_TW_SMEM_GC
+#define GW_TW_SMEM_GC 5  // smallest GC that keeps the lane twiddles in shared memory (none: TMEM measured faster at GC=4 too)
+#endif
+
 namespace gw {
 
 struct V3 {
@@ -50,7 +54,7 @@ struct V3 {
   static size_t smem_bytes(int gc, bool tma) {
     return (tma ? (size_t)SLAB : 0) +
            (size_t)gc * (UB * sizeof(double2) + 2 * N * sizeof(uint32_t) + XCHG * sizeof(uint32_t)) +
-           (gc >= 4 ? (size_t)P * L * sizeof(double2) : 0) + 128;
+           (gc >= GW_TW_SMEM_GC ? (size_t)P * L * sizeof(double2) : 0) + 128;
   }
 };
 
@@ -63,15 +67,19 @@ __host__ __device__ __forceinline__ size_t v3_index(int i, int cidx, int tlane) 
 
 // Lane twiddles streamed from TMEM eight at a time (register-lean variant for
 // GC >= 3): the transforms call tw(k1) for k1 = 0..15 in order.
+#ifndef GW_TW_CHUNK
+#define GW_TW_CHUNK 4  // complex twiddles per TMEM load in the register-lean variant (A/B: 4 > 2 > 8)
+#endif
 struct TwTmemHalves {
+  static constexpr int C = GW_TW_CHUNK;
   uint32_t taddr;
-  mutable uint32_t r[32];
+  mutable uint32_t r[4 * C];
   __device__ __forceinline__ double2 operator()(int k1) const {
-    if ((k1 & 7) == 0) {
-      tm_ld_raw<32>(taddr + (uint32_t)((k1 >> 3) * 32), r);
+    if (k1 % C == 0) {
+      tm_ld_raw<4 * C>(taddr + (uint32_t)((k1 / C) * 4 * C), r);
       tm_wait_ld();
     }
-    const uint32_t* w = r + (k1 & 7) * 4;
+    const uint32_t* w = r + (k1 % C) * 4;
     return make_double2(__hiloint2double(w[1], w[0]), __hiloint2double(w[3], w[2]));
   }
 };
@@ -121,7 +129,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
   uint32_t* acc_all = reinterpret_cast<uint32_t*>(ubuf_all + (size_t)GC * UB);
   uint32_t* xchg_all = acc_all + (size_t)GC * 2 * N;
   // GC = 4 (128 registers): lane twiddles from a shared-memory table; otherwise TMEM
-  constexpr bool kTwSmem = GC >= 4;
+  constexpr bool kTwSmem = GC >= GW_TW_SMEM_GC;
   double2* tw1 = reinterpret_cast<double2*>(xchg_all + (size_t)GC * V3::XCHG);
   uint64_t* bars = reinterpret_cast<uint64_t*>(tw1 + (kTwSmem ? P * L : 0));
   if constexpr (kTwSmem)

@@ -11,7 +11,7 @@ from paper_2306_11006_b200 import build as B  # noqa: E402
 name = sys.argv[1]
 os.makedirs(os.path.join(ROOT, "variants"), exist_ok=True)
 out = os.path.join(ROOT, "variants", f"lib_{name}.so")
-cmd = [B.nvcc(), *B.ARCH, *B.FLAGS, "-o", out, os.path.join(B.CSRC, "gw_api.cu")]
+cmd = [B.nvcc(), *B.ARCH, *B.FLAGS, *sys.argv[2:], "-o", out, os.path.join(B.CSRC, "gw_api.cu")]
 r = subprocess.run(cmd, capture_output=True, text=True)
 if r.returncode:
     sys.stderr.write(r.stdout + r.stderr)

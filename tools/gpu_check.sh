@@ -20,7 +20,7 @@ phase) for g in 128 256 296 592; do timeout 300 python tools/phase_profile.py $g
 phase2) for g in 256 592; do GATEWAVE_BR_KERNEL=v2 timeout 300 python tools/phase_profile.py $g; done > gpurun_out/${TAG}_phase2.txt 2>&1 ;;
 brtime) timeout 300 python tools/br_time.py > gpurun_out/${TAG}_brtime.txt 2>&1 ;;
 gcq) for gc in 1 2 4; do echo "GC=$gc"; GATEWAVE_BR_GC=$gc timeout 300 python tools/br_time.py 148 256 592 2368; done > gpurun_out/${TAG}_gcq.txt 2>&1 ;;
-ab) for v in $(ls variants/*.so); do for gc in 2 4; do echo "$v GC=$gc"; GATEWAVE_B200_LIB=$v GATEWAVE_BR_GC=$gc timeout 300 python tools/br_time.py 256 2368; done; done > gpurun_out/${TAG}_ab.txt 2>&1 ;;
+ab) for v in $(ls variants/*.so); do for gc in ${ABGC:-2 4}; do echo "$v GC=$gc"; GATEWAVE_B200_LIB=$v GATEWAVE_BR_GC=$gc timeout 300 python tools/br_time.py 256 2368; done; done > gpurun_out/${TAG}_ab.txt 2>&1 ;;
 gcsweep) for gc in 1 2 3 4; do echo "GC=$gc"; GATEWAVE_BR_GC=$gc timeout 300 python tools/br_time.py 148 256 444 592 1184 2368; done > gpurun_out/${TAG}_gcsweep.txt 2>&1 ;;
 esac
 done
