@@ -379,11 +379,22 @@ int launch_ks(gw_ctx* c, const uint32_t* acc, const KsUnit* units, int U, uint32
     k.blocks_per_split = (c->kt_kblocks + splits - 1) / splits;
     splits = (c->kt_kblocks + k.blocks_per_split - 1) / k.blocks_per_split;
     const size_t smem = (size_t)KT_STAGES * (KT_A_BYTES + KT_B_BYTES) + 256;
-    GW_CUDA(c, cudaFuncSetAttribute(k_keyswitch_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 grid(mt, c->kt_ntiles, splits);
-    k_keyswitch_tc<<<grid, KT_THREADS, smem, c->stream>>>(k);
-    GW_LAUNCHED(c);
-    return GW_OK;
+    auto go = [&](auto kern) -> int {
+      GW_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<grid, KT_THREADS, smem, c->stream>>>(k);
+      GW_LAUNCHED(c);
+      return GW_OK;
+    };
+    switch (c->p.ks_levels) {
+      case 1: return go(k_keyswitch_tc<1>);
+      case 2: return go(k_keyswitch_tc<2>);
+      case 4: return go(k_keyswitch_tc<4>);
+      case 8: return go(k_keyswitch_tc<8>);
+      case 16: return go(k_keyswitch_tc<16>);
+      case 32: return go(k_keyswitch_tc<32>);
+    }
+    return fail(c, GW_ERR_PARAM, "tensor-core keyswitch needs t | 32");
   }
   KsArgs a;
   a.acc = acc;

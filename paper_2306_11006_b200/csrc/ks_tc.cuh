@@ -84,6 +84,7 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
+template <int T>  // keyswitch levels t (divides 32): compile-time so the digit buffers stay in registers
 __global__ void __launch_bounds__(KT_THREADS, 1) k_keyswitch_tc(KtArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint8_t* sA = smem;                                   // [stage][kc 8][m 128][16]
@@ -155,11 +156,21 @@ __global__ void __launch_bounds__(KT_THREADS, 1) k_keyswitch_tc(KtArgs a) {
     const bool valid = g < a.count;
     const uint32_t dmask = (1u << a.gamma) - 1;
     const uint32_t* urow = a.ut + (valid ? g : 0);
+    // A K block spans KT_PAIRS / t input coefficients (t divides 32, so at most
+    // 32 when t = 1); the samples of block k+1 are loaded while block k is built,
+    // so the global-load latency overlaps the one-hot construction.
+    constexpr int UMAX = KT_PAIRS / T;  // coefficients per K block
+    uint32_t ucur[UMAX], unext[UMAX];
+    auto load_u = [&](int k, uint32_t (&dst)[UMAX]) {
+      const int c0 = ((kb0 + k) * KT_PAIRS) / T;
+#pragma unroll
+      for (int q = 0; q < UMAX; ++q)
+        dst[q] = (valid && k < nkb) ? __ldg(urow + (size_t)(c0 + q) * a.ut_stride) : 0u;
+    };
+    load_u(0, ucur);
     for (int k = 0; k < nkb; ++k) {
       const int s = k % KT_STAGES;
-      // the t digits of one input coefficient are consecutive pairs (t divides 32)
-      const int pair0 = (kb0 + k) * KT_PAIRS;
-      uint32_t u = 0;
+      load_u(k + 1, unext);
       mbar_wait(&empty[s], ((k / KT_STAGES) & 1) ^ 1);
       uint8_t* dst = sA + (size_t)s * KT_A_BYTES + m * 16;
 #pragma unroll
@@ -167,16 +178,18 @@ __global__ void __launch_bounds__(KT_THREADS, 1) k_keyswitch_tc(KtArgs a) {
         uint32_t w[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const int pair = pair0 + kc * 4 + e;
-          const int j = pair & (a.t - 1);
-          if (j == 0) u = valid ? __ldg(urow + (size_t)(pair / a.t) * a.ut_stride) : 0u;
-          const uint32_t d = (u >> ((a.t - 1 - j) * a.gamma)) & dmask;
+          const int pl = kc * 4 + e;  // pair within the block; pairs of a coefficient are consecutive
+          const int j = pl % T;
+          const uint32_t u = ucur[pl / T];
+          const uint32_t d = (u >> ((T - 1 - j) * a.gamma)) & dmask;
           w[e] = d ? (1u << (8 * (d - 1))) : 0u;
         }
         *reinterpret_cast<uint4*>(dst + kc * KT_M * 16) = make_uint4(w[0], w[1], w[2], w[3]);
       }
       fence_async_smem();
       mbar_arrive(&full_a[s]);
+#pragma unroll
+      for (int q = 0; q < UMAX; ++q) ucur[q] = unext[q];
     }
     // ---- epilogue: TMEM -> registers -> recombine planes -> atomics --------
     mbar_wait(done, 0);
