@@ -348,7 +348,7 @@ def run_ours(args):
     # the kernel the engine launches for this batch (gw_api.cu launch_v3: gates per CTA =
     # ceil(G / SMs), one CTA per SM; TMA key staging only at one gate per CTA)
     gc = min(4, max(1, -(-G // torch.cuda.get_device_properties(local).multi_processor_count)))
-    kname = f"k_blind_rotate_v3<{gc},{1 if gc == 1 else 0}>"
+    kname = f"k_blind_rotate_v3<{gc},{2 if gc == 1 else 0}>"
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:

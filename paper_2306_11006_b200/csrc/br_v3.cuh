@@ -111,8 +111,12 @@ __device__ __forceinline__ void tm_cp_128x256b(uint32_t taddr, uint64_t desc) {
 // + a shared-memory swap + a pair barrier) or done by every row warp alone
 constexpr bool kShareDigits = true;  // measured: sharing is 2-5 % faster
 
-template <int GC, bool TMA>
-__global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
+// KM = key streaming mode: 0 LDG by the compute warps, 1 TMA by warp 0, 2 four
+// dedicated loader warps (one per TMEM sub-partition; GC = 1 only).
+template <int GC, int KM>
+__global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rotate_v3(BrArgs a) {
+  constexpr bool TMA = KM == 1, LDR = KM == 2;
+  static_assert(!LDR || GC == 1, "loader warps need the register file of a one-gate CTA");
   using G = V3::G;
   constexpr int N = V3::N, M = V3::M, P = V3::P, L = V3::L, R = V3::R, LEV = V3::LEV, LOGN = V3::LOGN;
   constexpr int UB = V3::UB, COLS = V3::COLS, CIDX = V3::CIDX;
@@ -149,7 +153,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
 
   if (threadIdx.x == 0) {
     for (int k = 0; k < 2; ++k) {
-      mbar_init(&full_bar[k], TMA ? 1 : 4 * GC);
+      mbar_init(&full_bar[k], TMA ? 1 : LDR ? 4 : 4 * GC);
       mbar_init(&empty_bar[k], 4 * GC);
     }
     mbar_init(stage_bar, 1);
@@ -183,7 +187,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
   double2 kb[GPP][8];
   // LDG mode, phase point pt of step i: load / store this warp's groups
   auto kissue = [&](int i, int pt) {
-    if constexpr (!TMA) {
+    if constexpr (KM == 0) {
       const double2* src = kw_base + (size_t)i * CIDX * 128;
 #pragma unroll
       for (int gg = 0; gg < GPP; ++gg) {
@@ -197,7 +201,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
   // store for step i+1 (ring base slot sn); its chunk 3 reuses the slot of step i's
   // chunk 0, so it waits until every warp has finished MAC(i) (empty barrier of step i)
   auto kstore = [&](int i, int sn, int pt) {
-    if constexpr (!TMA) {
+    if constexpr (KM == 0) {
 #pragma unroll
       for (int gg = 0; gg < GPP; ++gg) {
         const int j = pt * GPP + gg, grp = gl + GC * j;
@@ -235,7 +239,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
       mbar_wait(stage_bar, 0);
       copy_to_tmem(0, 0);
     }
-  } else {
+  } else if constexpr (KM == 0) {
     for (int pt = 0; pt < 4; ++pt) {  // prologue: slab 0 -> ring slots 0..3 (no chunk-3 wait)
       kissue(0, pt);
 #pragma unroll
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
   uint32_t* acc_g = acc_all + (size_t)gl * 2 * N;
   double2* U = ubuf_all + (size_t)gl * UB;
   // acc <- tv * X^{-bbar} (cggi.py:612-622): warp o < 2 initialises component o
-  if (o < 2) {
+  if (warp < 4 * GC && o < 2) {
     const uint32_t bbar = ((lin_g[a.n] + radd) >> rshift) & two_n_mask;
     const uint32_t k = (2 * N - bbar) & two_n_mask;
     const uint32_t* tvc = a.tv + o * N;
@@ -302,6 +306,43 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
     }
   };
 
+  if (LDR && warp >= 4 * GC) {
+    // ---- loader warp: slab i -> ring slots of sub-partition o, ahead of the MAC ----
+    const double2* src_w = a.bk + (size_t)32 * o + lane;
+    int s_i = 0;
+    for (int i = 0; i < a.n; ++i) {
+      const double2* src = src_w + (size_t)i * CIDX * 128;
+      if (i >= 2) {  // chunks 0-2 reuse the slots of slab i-2's chunks 1-3
+        mbar_wait(&empty_bar[i & 1], (uint32_t)(((i - 2) >> 1) & 1));
+        tm_fence_after();
+      }
+#pragma unroll 1
+      for (int rnd = 0; rnd < 2; ++rnd) {
+        double2 v[24];
+#pragma unroll
+        for (int k = 0; k < 24; ++k) v[k] = ldg_stream(src + (size_t)(rnd * 24 + k) * 128);
+#pragma unroll
+        for (int k = 0; k < 24; ++k) {
+          const int cidx = rnd * 24 + k;
+          tm_st4(tm_warp + kcol(s_i, cidx >> 4) + (uint32_t)((cidx & 15) * 4), v[k]);
+        }
+      }
+      if (i >= 1) {  // chunk 3 reuses the slot of slab i-1's chunk 0
+        mbar_wait(&empty_bar[(i - 1) & 1], (uint32_t)(((i - 1) >> 1) & 1));
+        tm_fence_after();
+      }
+      {
+        double2 v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = ldg_stream(src + (size_t)(48 + k) * 128);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) tm_st4(tm_warp + kcol(s_i, 3) + (uint32_t)(k * 4), v[k]);
+      }
+      tm_wait_st();
+      release(&full_bar[i & 1]);
+      s_i = s_i + 4 >= V3::RING ? s_i + 4 - V3::RING : s_i + 4;
+    }
+  } else {
   uint32_t a_next = __ldg(lin_g);
   for (int i = 0; i < a.n; ++i) {
     const int cur = i & 1, nxt = cur ^ 1;
@@ -397,7 +438,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
       for (int c = 0; c < P; ++c) tile[c * L + pos] = x[c];
     }
     mark(0);
-    if (!TMA && pre) {  // buffer nxt is free once every warp finished MAC(i-1)
+    if (KM == 0 && pre) {  // buffer nxt is free once every warp finished MAC(i-1)
       if (i >= 1) mbar_wait(&empty_bar[nxt], (uint32_t)(((i - 1) >> 1) & 1));
       tm_fence_after();
       kstore(i, sn, 0);
@@ -489,7 +530,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
       }
     }
     mark(4);
-    if (!TMA && pre) {
+    if (KM == 0 && pre) {
       kstore(i, sn, 3);
       tm_wait_st();
       release(&full_bar[nxt]);
@@ -514,6 +555,7 @@ __global__ void __launch_bounds__(128 * GC, 1) k_blind_rotate_v3(BrArgs a) {
     uint32_t* dst = a.acc_out + ((size_t)g * 2 + o) * N;
     for (int j = lane; j < N; j += 32) dst[j] = acc_g[o * N + j];
   }
+  }  // compute warps
   tm_fence_before();
   __syncthreads();
   if (warp == 0) tm_dealloc(tm_base, 512);

@@ -88,6 +88,7 @@ struct gw_ctx {
   // 1: v2 TMEM 4-warp kernel, 0: v1 2-warp kernel (GATEWAVE_BR_KERNEL=v3|v2|v1)
   int br_variant = 2;
   int br_gc = 0;  // v3 gates per CTA override (GATEWAVE_BR_GC, measurement only; 0 = by batch size)
+  bool br_gc1_tma = false;  // GATEWAVE_BR_GC1=tma: one-gate CTAs stage the key through shared memory
   std::string err;
 };
 
@@ -265,28 +266,30 @@ int launch_tm(gw_ctx* c, const BrArgs& a) {
   return rc;
 }
 
-template <int GC, bool TMA>
+template <int GC, int KM>
 int launch_v3_g(gw_ctx* c, const BrArgs& a0) {
   BrArgs a = a0;
   a.bk = c->bk_v3;
-  const size_t smem = V3::smem_bytes(GC, TMA);
-  GW_CUDA(c, cudaFuncSetAttribute(k_blind_rotate_v3<GC, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem = V3::smem_bytes(GC, KM == 1);
+  GW_CUDA(c, cudaFuncSetAttribute(k_blind_rotate_v3<GC, KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
   a.gates_per_cta = GC;
   const int grid = (a.B + GC - 1) / GC;
-  k_blind_rotate_v3<GC, TMA><<<grid, 128 * GC, smem, c->stream>>>(a);
+  k_blind_rotate_v3<GC, KM><<<grid, 128 * GC + (KM == 2 ? 128 : 0), smem, c->stream>>>(a);
   GW_LAUNCHED(c);
   return GW_OK;
 }
 
-// v3: one CTA per SM; two gates per CTA once the batch exceeds one per SM.
+// v3: one CTA per SM; gates per CTA = ceil(B / SMs) up to 4.  One gate per CTA
+// streams the key with four dedicated loader warps (GATEWAVE_BR_GC1=tma: the
+// bulk-copy + tcgen05.cp staging path).
 int launch_v3(gw_ctx* c, const BrArgs& a) {
   int gc = (int)((a.B + c->sm_count - 1) / c->sm_count);
   if (c->br_gc > 0) gc = c->br_gc;
-  if (gc >= 4) return launch_v3_g<4, false>(c, a);
-  if (gc == 3) return launch_v3_g<3, false>(c, a);
-  if (gc == 2) return launch_v3_g<2, false>(c, a);
-  return launch_v3_g<1, true>(c, a);
+  if (gc >= 4) return launch_v3_g<4, 0>(c, a);
+  if (gc == 3) return launch_v3_g<3, 0>(c, a);
+  if (gc == 2) return launch_v3_g<2, 0>(c, a);
+  return c->br_gc1_tma ? launch_v3_g<1, 1>(c, a) : launch_v3_g<1, 2>(c, a);
 }
 
 template <int LOGN>
@@ -604,6 +607,7 @@ int gw_create(int device, gw_ctx** out) {
   if (!rc && (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess)) rc = GW_ERR_CUDA;
   if (!rc) rc = upload_roots(c);
   if (const char* v = getenv("GATEWAVE_BR_GC")) c->br_gc = atoi(v);
+  if (const char* v = getenv("GATEWAVE_BR_GC1")) c->br_gc1_tma = strcmp(v, "tma") == 0;
   if (const char* v = getenv("GATEWAVE_BR_KERNEL"))
     c->br_variant = strcmp(v, "v1") == 0 ? 0 : strcmp(v, "v2") == 0 ? 1 : 2;
   if (const char* v = getenv("GATEWAVE_KS_KERNEL")) c->ks_variant = strcmp(v, "cuda") == 0 ? 0 : 1;
