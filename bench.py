@@ -345,10 +345,12 @@ def run_ours(args):
     flops_per_bootstrap = 249_856 * P.n                      # SURVEY.md §8(d), FP64 path
     achieved = flops_per_bootstrap * br_items / (br_ms / 1e3) / 1e12 if br_ms > 0 else 0.0
     bk_bytes = P.n * 2 * (2 * P.l) * 2 * (P.N // 2) * 16    # FFT-domain key, one pass
-    # the kernel the engine launches for this batch (gw_api.cu launch_v3: gates per CTA =
-    # ceil(G / SMs), one CTA per SM; TMA key staging only at one gate per CTA)
-    gc = min(4, max(1, -(-G // torch.cuda.get_device_properties(local).multi_processor_count)))
-    kname = f"k_blind_rotate_v3<{gc},{2 if gc == 1 else 0}>"
+    # the kernel the engine launches for this batch (gw_api.cu launch_v3: gates per CTA
+    # minimising waves x measured step time; loader-warp key streaming below 4 per CTA)
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    step_kcyc = {1: 7.8, 2: 9.6, 3: 12.8, 4: 17.7}   # gw_api.cu launch_v3 policy
+    gc = min(step_kcyc, key=lambda g: (-(-G // (sms * g)) * step_kcyc[g], g))
+    kname = f"k_blind_rotate_v3<{gc},{0 if gc == 4 else 2}>"
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:

@@ -116,7 +116,11 @@ constexpr bool kShareDigits = true;  // measured: sharing is 2-5 % faster (DESIG
 template <int GC, int KM>
 __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rotate_v3(BrArgs a) {
   constexpr bool TMA = KM == 1, LDR = KM == 2;
-  static_assert(!LDR || GC == 1, "loader warps need the register file of a one-gate CTA");
+  static_assert(!LDR || GC <= 3, "loader warps need registers the compute warps can spare");
+  // with loader warps at GC >= 2 the register file is re-split with setmaxnreg:
+  // compute warpgroups CREG, the loader warpgroup LREG (CREG*128*GC + LREG*128 <= 64K)
+  constexpr int LREG = GC == 1 ? 0 : GC == 2 ? 64 : 56;
+  constexpr int CREG = GC == 1 ? 0 : GC == 2 ? 216 : 152;
   using G = V3::G;
   constexpr int N = V3::N, M = V3::M, P = V3::P, L = V3::L, R = V3::R, LEV = V3::LEV, LOGN = V3::LOGN;
   constexpr int UB = V3::UB, COLS = V3::COLS, CIDX = V3::CIDX;
@@ -308,6 +312,8 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
 
   if (LDR && warp >= 4 * GC) {
     // ---- loader warp: slab i -> ring slots of sub-partition o, ahead of the MAC ----
+    if constexpr (LDR && GC >= 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(LREG));
+    constexpr int RS = GC == 1 ? 24 : 16;  // loads in flight per round
     const double2* src_w = a.bk + (size_t)32 * o + lane;
     int s_i = 0;
     for (int i = 0; i < a.n; ++i) {
@@ -317,13 +323,13 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
         tm_fence_after();
       }
 #pragma unroll 1
-      for (int rnd = 0; rnd < 2; ++rnd) {
-        double2 v[24];
+      for (int rnd = 0; rnd < 48 / RS; ++rnd) {
+        double2 v[RS];
 #pragma unroll
-        for (int k = 0; k < 24; ++k) v[k] = ldg_stream(src + (size_t)(rnd * 24 + k) * 128);
+        for (int k = 0; k < RS; ++k) v[k] = ldg_stream(src + (size_t)(rnd * RS + k) * 128);
 #pragma unroll
-        for (int k = 0; k < 24; ++k) {
-          const int cidx = rnd * 24 + k;
+        for (int k = 0; k < RS; ++k) {
+          const int cidx = rnd * RS + k;
           tm_st4(tm_warp + kcol(s_i, cidx >> 4) + (uint32_t)((cidx & 15) * 4), v[k]);
         }
       }
@@ -343,6 +349,7 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
       s_i = s_i + 4 >= V3::RING ? s_i + 4 - V3::RING : s_i + 4;
     }
   } else {
+  if constexpr (LDR && GC >= 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(CREG));
   uint32_t a_next = __ldg(lin_g);
   for (int i = 0; i < a.n; ++i) {
     const int cur = i & 1, nxt = cur ^ 1;

@@ -88,7 +88,8 @@ struct gw_ctx {
   // 1: v2 TMEM 4-warp kernel, 0: v1 2-warp kernel (GATEWAVE_BR_KERNEL=v3|v2|v1)
   int br_variant = 2;
   int br_gc = 0;  // v3 gates per CTA override (GATEWAVE_BR_GC, measurement only; 0 = by batch size)
-  bool br_gc1_tma = false;  // GATEWAVE_BR_GC1=tma: one-gate CTAs stage the key through shared memory
+  bool br_gc1_tma = false;
+  bool br_ldr = true;  // loader warps at GC = 2, 3 (GATEWAVE_BR_LDR=0: LDG by the compute warps)  // GATEWAVE_BR_GC1=tma: one-gate CTAs stage the key through shared memory
   std::string err;
 };
 
@@ -280,15 +281,26 @@ int launch_v3_g(gw_ctx* c, const BrArgs& a0) {
   return GW_OK;
 }
 
-// v3: one CTA per SM; gates per CTA = ceil(B / SMs) up to 4.  One gate per CTA
-// streams the key with four dedicated loader warps (GATEWAVE_BR_GC1=tma: the
-// bulk-copy + tcgen05.cp staging path).
+// v3: one CTA per SM holding GC gates.  GC minimises waves x step time, with the
+// measured per-step cycles of each configuration (profiles/r01_v3_gc_sweep.txt):
+// GC=1 7.8k (loader warps), GC=2 9.6k, GC=3 12.8k (loader warps + setmaxnreg),
+// GC=4 17.7k (LDG key streaming by the compute warps).
 int launch_v3(gw_ctx* c, const BrArgs& a) {
-  int gc = (int)((a.B + c->sm_count - 1) / c->sm_count);
+  static const double kStep[5] = {0, 7.8, 9.6, 12.8, 17.7};
+  int gc = 1;
+  double best = 1e300;
+  for (int g = 1; g <= 4; ++g) {
+    const double waves = (double)((a.B + (int64_t)c->sm_count * g - 1) / ((int64_t)c->sm_count * g));
+    const double t = waves * kStep[g];
+    if (t < best * 0.999) {
+      best = t;
+      gc = g;
+    }
+  }
   if (c->br_gc > 0) gc = c->br_gc;
   if (gc >= 4) return launch_v3_g<4, 0>(c, a);
-  if (gc == 3) return launch_v3_g<3, 0>(c, a);
-  if (gc == 2) return launch_v3_g<2, 0>(c, a);
+  if (gc == 3) return c->br_ldr ? launch_v3_g<3, 2>(c, a) : launch_v3_g<3, 0>(c, a);
+  if (gc == 2) return c->br_ldr ? launch_v3_g<2, 2>(c, a) : launch_v3_g<2, 0>(c, a);
   return c->br_gc1_tma ? launch_v3_g<1, 1>(c, a) : launch_v3_g<1, 2>(c, a);
 }
 
@@ -608,6 +620,7 @@ int gw_create(int device, gw_ctx** out) {
   if (!rc) rc = upload_roots(c);
   if (const char* v = getenv("GATEWAVE_BR_GC")) c->br_gc = atoi(v);
   if (const char* v = getenv("GATEWAVE_BR_GC1")) c->br_gc1_tma = strcmp(v, "tma") == 0;
+  if (const char* v = getenv("GATEWAVE_BR_LDR")) c->br_ldr = atoi(v) != 0;
   if (const char* v = getenv("GATEWAVE_BR_KERNEL"))
     c->br_variant = strcmp(v, "v1") == 0 ? 0 : strcmp(v, "v2") == 0 ? 1 : 2;
   if (const char* v = getenv("GATEWAVE_KS_KERNEL")) c->ks_variant = strcmp(v, "cuda") == 0 ? 0 : 1;
@@ -893,8 +906,8 @@ int gw_keyswitch(gw_ctx* c, const uint32_t* ext, int64_t B, uint32_t* out) {
   return GW_OK;
 }
 
-static int eval_stacked(gw_ctx* c, int opcode, const uint32_t* stacked, int arity, int64_t B, uint32_t* d_out,
-                        int64_t out_stride) {
+static int eval_stacked(gw_ctx* c, int opcode, const uint32_t* stacked, int64_t in_stride, int arity, int64_t B,
+                        uint32_t* d_out, int64_t out_stride) {
   // Descriptors of a homogeneous batch depend only on (opcode, B): cache them
   // on the device so repeated batches enqueue without any host round trip.
   const uint64_t key = ((uint64_t)opcode << 40) | (uint64_t)B;
@@ -931,7 +944,7 @@ static int eval_stacked(gw_ctx* c, int opcode, const uint32_t* stacked, int arit
     it = c->batch_desc.emplace(key, d).first;
   }
   const BatchDesc& d = it->second;
-  return run_level(c, stacked, c->Wp, d_out, out_stride, d.jobs, d.J, d.units, d.U, d.cheap, d.C);
+  return run_level(c, stacked, in_stride, d_out, out_stride, d.jobs, d.J, d.units, d.U, d.cheap, d.C);
 }
 
 static int check_batch(gw_ctx* c, int opcode, int arity, int64_t B) {
@@ -970,7 +983,7 @@ int gw_eval_gate_batch_device(gw_ctx* c, int opcode, const uint32_t* const* d_op
       stacked = c->io;
     }
   }
-  return eval_stacked(c, opcode, stacked, arity, B, d_out, out_stride);
+  return eval_stacked(c, opcode, stacked, c->Wp, arity, B, d_out, out_stride);
 }
 
 int gw_eval_gate_batch(gw_ctx* c, int opcode, const uint32_t* const* ops, int arity, int64_t B, uint32_t* out) {
@@ -981,16 +994,17 @@ int gw_eval_gate_batch(gw_ctx* c, int opcode, const uint32_t* const* ops, int ar
     if (!ops[k]) return fail(c, GW_ERR_ARG, "null operand");
   if (!out) return fail(c, GW_ERR_ARG, "null output");
   cudaSetDevice(c->device);
+  // Host rows are copied as they are (unpadded, stride W): one contiguous DMA per
+  // operand and one for the result; the gate kernels take any row stride.
   const int W = c->p.n + 1;
-  const size_t in_words = (size_t)arity * B * c->Wp;
-  if ((rc = ensure(c, &c->io, &c->io_cap, in_words + (size_t)B * c->Wp, sizeof(uint32_t)))) return rc;
+  const size_t in_words = (size_t)arity * B * W;
+  if ((rc = ensure(c, &c->io, &c->io_cap, in_words + (size_t)B * W, sizeof(uint32_t)))) return rc;
   for (int k = 0; k < arity; ++k)
-    GW_CUDA(c, cudaMemcpy2DAsync(c->io + (size_t)k * B * c->Wp, c->Wp * sizeof(uint32_t), ops[k],
-                                 W * sizeof(uint32_t), W * sizeof(uint32_t), B, cudaMemcpyHostToDevice, c->stream));
+    GW_CUDA(c, cudaMemcpyAsync(c->io + (size_t)k * B * W, ops[k], (size_t)B * W * sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, c->stream));
   uint32_t* dout = c->io + in_words;
-  if ((rc = eval_stacked(c, opcode, c->io, arity, B, dout, c->Wp))) return rc;
-  GW_CUDA(c, cudaMemcpy2DAsync(out, W * sizeof(uint32_t), dout, c->Wp * sizeof(uint32_t), W * sizeof(uint32_t), B,
-                               cudaMemcpyDeviceToHost, c->stream));
+  if ((rc = eval_stacked(c, opcode, c->io, W, arity, B, dout, W))) return rc;
+  GW_CUDA(c, cudaMemcpyAsync(out, dout, (size_t)B * W * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
   GW_CUDA(c, cudaStreamSynchronize(c->stream));
   return GW_OK;
 }
@@ -1092,8 +1106,8 @@ int gw_plan_create(gw_ctx* c, int64_t n_levels, const int64_t* offs, const int32
   // Every level is cut into segments of at most kSegGates gates (the gates of
   // a level are independent): a segment is one launch set, so scratch memory
   // stays bounded (~1 GB) however wide the level is.  kSegGates is a multiple
-  // of 148 SMs x 4 gates per CTA, i.e. whole waves of the blind rotation.
-  constexpr int64_t kSegGates = 148 * 4 * 28;
+  // of 148 SMs x 3 and x 4 gates per CTA, i.e. whole waves of the blind rotation.
+  constexpr int64_t kSegGates = 148 * 12 * 9;  // whole waves at 3 and 4 gates per CTA
   for (int64_t lv = 0; lv < n_levels; ++lv) {
    p->seg_first.push_back((int64_t)p->J.size());
    for (int64_t s0 = offs[lv]; s0 < offs[lv + 1] || s0 == offs[lv]; s0 += kSegGates) {

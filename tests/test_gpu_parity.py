@@ -87,7 +87,7 @@ def test_config1_digest_p128(engine_mod, golden_json, golden_p128, p128_keys):
     assert np.array_equal(decrypt_rows(p128_keys.lwe_sk, out), (1 - (bits_a & bits_b)).astype(np.uint8))
 
 
-@pytest.mark.parametrize("batch", [1, 150, 300, 600])
+@pytest.mark.parametrize("batch", [1, 150, 300, 592, 600])  # gates per CTA 1, 2, 3, 4, 3
 def test_blind_rotate_batch_shapes_p128(engine_mod, p128_keys, batch):
     """Every CTA geometry (1, 2 or 4 gates per CTA, partial last CTA) against
     the oracle on sampled rows of random LWE samples and a random test vector."""
@@ -124,3 +124,29 @@ def test_two_kernel_variants_agree_p128(engine_mod, p128_keys):
         del os.environ["GATEWAVE_BR_KERNEL"]
     b.upload_keys(ks.bootstrapping_key.data, ks.keyswitch_key.data)
     assert np.array_equal(a.blind_rotate(lin, tv), b.blind_rotate(lin, tv))
+
+
+@pytest.mark.parametrize("mode", [{"GATEWAVE_BR_GC": "1", "GATEWAVE_BR_GC1": "tma"},
+                                  {"GATEWAVE_BR_GC": "2", "GATEWAVE_BR_LDR": "0"},
+                                  {"GATEWAVE_BR_GC": "3", "GATEWAVE_BR_LDR": "0"},
+                                  {"GATEWAVE_BR_GC": "4"},
+                                  {"GATEWAVE_BR_KERNEL": "v2"}])
+def test_blind_rotate_alternative_kernels_p128(engine_mod, p128_keys, mode, monkeypatch):
+    """The non-default blind-rotation configurations (key staging through shared
+    memory, key streaming by the compute warps, forced gates-per-CTA, the v2
+    kernel) are bit-exact too; a fresh context reads the overrides."""
+    import oracle as O
+    from paper_2306_11006_b200.cggi import PARAM_128
+    from paper_2306_11006_b200.engine import Engine, params_tuple
+    for k, v in mode.items():
+        monkeypatch.setenv(k, v)
+    eng = Engine(*params_tuple(PARAM_128), device=0)
+    eng.upload_keys(p128_keys.bootstrapping_key.data, None)
+    rng = np.random.default_rng(7)
+    lin = rng.integers(0, 2 ** 32, (200, PARAM_128.n + 1), dtype=np.uint32)
+    tv = rng.integers(0, 2 ** 32, (2, PARAM_128.N), dtype=np.uint32)
+    acc = eng.blind_rotate(lin, tv)
+    okeys = O.Keys.from_params(PARAM_128, p128_keys.bootstrapping_key.data, p128_keys.keyswitch_key.data)
+    rows = [0, 77, 199]
+    want = O.blind_rotate(lin[rows], tv, okeys.bk_ntt, okeys.bg_bits, okeys.l, 8)
+    assert np.array_equal(acc[rows], want)
