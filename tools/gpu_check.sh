@@ -14,7 +14,7 @@ benchq) timeout 600 python bench.py --no-cpu-baseline --no-netlist > gpurun_out/
 ref) timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${TAG}_ref.json 2> gpurun_out/${TAG}_ref.err ;;
 launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-netlist > gpurun_out/${TAG}_launches.log 2>&1 ;;
 ncu) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_blind_rotate -s 1 -c 1 -o gpurun_out/${TAG}_br -f python tools/br_once.py 256 > gpurun_out/${TAG}_ncu.log 2>&1 ;;
-ncu4) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_blind_rotate -s 1 -c 1 -o gpurun_out/${TAG}_br592 -f python tools/br_once.py 592 > gpurun_out/${TAG}_ncu4.log 2>&1 ;;
+ncu4) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_blind_rotate -s 1 -c 1 -o gpurun_out/${TAG}_br592 -f python tools/br_once.py 592; timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_blind_rotate -s 1 -c 1 -o gpurun_out/${TAG}_br444 -f python tools/br_once.py 444 > gpurun_out/${TAG}_ncu4.log 2>&1 ;;
 ncuks) timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_keyswitch_tc -s 1 -c 1 -o gpurun_out/${TAG}_ks -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-netlist > gpurun_out/${TAG}_ncuks.log 2>&1 ;;
 phase) for g in 128 256 296 592; do timeout 300 python tools/phase_profile.py $g; done > gpurun_out/${TAG}_phase.txt 2>&1 ;;
 phase2) for g in 256 592; do GATEWAVE_BR_KERNEL=v2 timeout 300 python tools/phase_profile.py $g; done > gpurun_out/${TAG}_phase2.txt 2>&1 ;;
