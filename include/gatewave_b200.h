@@ -57,6 +57,14 @@ typedef struct gw_ctx gw_ctx;
 typedef struct gw_plan gw_plan;
 
 int gw_version(void);
+
+/* Host-only netlist helper (no GPU needed), replaces the FIFO level walk of
+ * gatewave/scheduler.py:57-102 (partition_waves) for 10^7-gate netlists:
+ * pos[3*k + j] is the gate POSITION (index in execution order) of operand j of
+ * gate k, or -1 for a circuit input / unused slot; level[k] = 1 + max level of
+ * its gate operands (0 if none).  Returns GW_ERR_ARG if an operand position is
+ * not strictly before k (not a sequential form). */
+int gw_levels(const int64_t* pos, int64_t gates, int32_t* level);
 int gw_device_count(int* count);
 
 /* Context life cycle.  `device` is the CUDA ordinal. */

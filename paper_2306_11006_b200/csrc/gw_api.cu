@@ -591,6 +591,21 @@ extern "C" {
 
 int gw_version(void) { return 1; }
 
+int gw_levels(const int64_t* pos, int64_t gates, int32_t* level) {
+  if (gates < 0 || (gates > 0 && (!pos || !level))) return GW_ERR_ARG;
+  for (int64_t k = 0; k < gates; ++k) {
+    int32_t m = -1;
+    for (int j = 0; j < 3; ++j) {
+      const int64_t p = pos[3 * k + j];
+      if (p < 0) continue;
+      if (p >= k) return GW_ERR_ARG;
+      if (level[p] > m) m = level[p];
+    }
+    level[k] = m + 1;
+  }
+  return GW_OK;
+}
+
 int gw_device_count(int* count) {
   if (!count) return GW_ERR_ARG;
   if (cudaGetDeviceCount(count) != cudaSuccess) {

@@ -30,7 +30,7 @@ OPCODES = {"AND": 0, "OR": 1, "NAND": 2, "NOR": 3, "XOR": 4, "XNOR": 5, "NOT": 6
            "CONST0": 8, "CONST1": 9, "COPY": 10, "BOOTSTRAP": 11}
 
 # Every symbol include/gatewave_b200.h declares.
-EXPORTS = ("gw_version", "gw_device_count", "gw_create", "gw_destroy", "gw_last_error",
+EXPORTS = ("gw_version", "gw_levels", "gw_device_count", "gw_create", "gw_destroy", "gw_last_error",
            "gw_set_stream", "gw_sync", "gw_set_params", "gw_upload_keys", "gw_bk_fft_size",
            "gw_download_bk_fft", "gw_blind_rotate", "gw_keyswitch", "gw_eval_gate_batch",
            "gw_eval_gate_batch_device", "gw_wires_alloc", "gw_wires_put", "gw_wires_get",
@@ -71,6 +71,7 @@ def load_library(path: str | None = None):
         L = ctypes.CDLL(path)
         sig = {
             "gw_version": ([], ctypes.c_int),
+            "gw_levels": ([_I64P, ctypes.c_int64, ctypes.POINTER(ctypes.c_int32)], ctypes.c_int),
             "gw_device_count": ([ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
             "gw_create": ([ctypes.c_int, ctypes.POINTER(_P)], ctypes.c_int),
             "gw_destroy": ([_P], ctypes.c_int),

@@ -22,10 +22,14 @@ shallow, wide levels, which is the shape that keeps many gates per level.
 """
 from __future__ import annotations
 
+import numpy as np
+
 from .cggi import GateKind
 from .circuit import Circuit, Gate, Port
 
 _K = GateKind
+_CODE = {k: i for i, k in enumerate(GateKind)}  # scheduler._OPC order
+_PAD = {0: (-1, -1, -1), 1: (-1, -1), 2: (-1,), 3: ()}
 
 
 class NetBuilder:
@@ -37,6 +41,9 @@ class NetBuilder:
         self.gates: list[Gate] = []
         self.nxt = 0
         self._const: dict[int, int] = {}
+        # flat copies for the scheduler / plan compiler (scheduler.circuit_arrays)
+        self._codes: list[int] = []
+        self._ops: list[int] = []
 
     def add_input(self, name: str, width: int) -> list[int]:
         if self.gates:
@@ -51,6 +58,8 @@ class NetBuilder:
 
     def gate(self, op: GateKind, *ops: int) -> int:
         self.gates.append(Gate(self.nxt, op, tuple(ops)))
+        self._codes.append(_CODE[op])
+        self._ops.extend(ops + _PAD[len(ops)])
         self.nxt += 1
         return self.nxt - 1
 
@@ -60,8 +69,13 @@ class NetBuilder:
         return self._const[bit]
 
     def build(self) -> Circuit:
-        return Circuit(inputs=tuple(self.inputs), outputs=tuple(self.outputs),
-                       gates=tuple(self.gates))
+        c = Circuit(inputs=tuple(self.inputs), outputs=tuple(self.outputs), gates=tuple(self.gates))
+        G = len(self.gates)
+        ids = np.fromiter((g.id for g in self.gates), dtype=np.int64, count=G)
+        ops = np.asarray(self._ops, dtype=np.int64).reshape(G, 3)
+        c.__dict__["_plan_arrays"] = (ids, np.asarray(self._codes, dtype=np.int32), ops,
+                                      (ops >= 0).sum(axis=1).astype(np.int32))
+        return c
 
     # -- bit-level blocks ------------------------------------------------------
     def full_add(self, a, b, c):

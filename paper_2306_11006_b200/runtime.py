@@ -127,20 +127,8 @@ class LevelPlan:
 
 
 def _circuit_arrays(c: Circuit):
-    """(ids, opcode codes, operands (G, 3) -1 padded, arity) in circuit order,
-    cached on the circuit (one pass over the Gate objects)."""
-    cached = c.__dict__.get("_plan_arrays")
-    if cached is not None:
-        return cached
-    G = len(c.gates)
-    ids = np.fromiter((g.id for g in c.gates), dtype=np.int64, count=G)
-    kinds = [as_kind(g.opcode) for g in c.gates]
-    codes = np.fromiter((_OPC[k.value] for k in kinds), dtype=np.int32, count=G)
-    ar = np.fromiter((len(g.operands) for g in c.gates), dtype=np.int32, count=G)
-    flat = np.fromiter((w for g in c.gates for w in (*g.operands, -1, -1, -1)[:3]), dtype=np.int64, count=3 * G)
-    out = (ids, codes, flat.reshape(G, 3), ar)
-    c.__dict__["_plan_arrays"] = out
-    return out
+    from .scheduler import circuit_arrays
+    return circuit_arrays(c)
 
 
 _ARITY_OF_CODE = np.array([GATE_ARITY[as_kind(k)] for k in _OPC], dtype=np.int32)

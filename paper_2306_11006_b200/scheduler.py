@@ -52,15 +52,25 @@ class Schedule:
         return sum(len(w) for w in self.waves)
 
 
-def gate_arrays(c: Circuit):
-    """(ids, opcodes, operands (G,3) with -1 padding) as numpy arrays."""
+def circuit_arrays(c: Circuit):
+    """(ids, opcode codes, operands (G, 3) -1 padded, arity) in circuit order,
+    built in one pass over the Gate objects and cached on the circuit."""
+    cached = c.__dict__.get("_plan_arrays")
+    if cached is not None:
+        return cached
     G = len(c.gates)
     ids = np.fromiter((g.id for g in c.gates), dtype=np.int64, count=G)
     codes = np.fromiter((_OPC[as_kind(g.opcode)] for g in c.gates), dtype=np.int32, count=G)
-    opnd = np.full((G, 3), -1, dtype=np.int64)
-    for k, g in enumerate(c.gates):
-        for j, w in enumerate(g.operands):
-            opnd[k, j] = w
+    ar = np.fromiter((len(g.operands) for g in c.gates), dtype=np.int32, count=G)
+    flat = np.fromiter((w for g in c.gates for w in (*g.operands, -1, -1, -1)[:3]), dtype=np.int64, count=3 * G)
+    out = (ids, codes, flat.reshape(G, 3), ar)
+    c.__dict__["_plan_arrays"] = out
+    return out
+
+
+def gate_arrays(c: Circuit):
+    """(ids, opcodes, operands (G,3) with -1 padding) as numpy arrays."""
+    ids, codes, opnd, _ = circuit_arrays(c)
     return ids, codes, opnd
 
 
@@ -68,36 +78,53 @@ _KINDS = list(GateKind)
 _OPC = {k: i for i, k in enumerate(_KINDS)}
 
 
+def _levels_native(pos: np.ndarray):
+    """gw_levels from the engine library (host code, no GPU); None if unavailable."""
+    try:
+        import ctypes
+        from .engine import load_library
+        lib = load_library()
+    except Exception:
+        return None
+    pos = np.ascontiguousarray(pos, dtype=np.int64)
+    lv = np.empty(pos.shape[0], dtype=np.int32)
+    rc = lib.gw_levels(pos.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), pos.shape[0],
+                       lv.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)))
+    return lv.astype(np.int64) if rc == 0 else None
+
+
 def wave_index(c: Circuit) -> np.ndarray:
     """Longest-path level of every gate (same rule as the reference's FIFO
     walk: level = 1 + max level of gate operands, 0 if only inputs feed it).
 
-    Gates are in SSA execution order, so one pass in gate order suffices;
-    operands that are not gate outputs (circuit inputs) contribute nothing.
+    Gates are in SSA execution order, so one pass in gate order suffices
+    (native `gw_levels` when the engine library is present); operands that are
+    not gate outputs (circuit inputs) contribute nothing.
     """
-    ids, _, opnd = gate_arrays(c)
+    ids, _, opnd, _ = circuit_arrays(c)
     if len(ids) == 0:
         return np.zeros(0, dtype=np.int64)
     top = int(max(ids.max(), opnd.max(), c.max_wire)) + 1
-    level_of_wire = np.full(top + 1, -1, dtype=np.int64)  # -1: input / undefined
     pos_of_wire = np.full(top + 1, -1, dtype=np.int64)
     pos_of_wire[ids] = np.arange(len(ids))
-    lv = np.zeros(len(ids), dtype=np.int64)
+    pos = np.where(opnd >= 0, pos_of_wire[np.where(opnd >= 0, opnd, top)], -1)
     # SSA order check: an operand defined by a LATER gate means not sequential
+    late = pos >= np.arange(len(ids))[:, None]
+    if late.any():
+        k = int(np.argwhere(late)[0][0])
+        w = int(opnd[k][np.argmax(late[k])])
+        raise SchedulerError("circuit is not a valid sequential form: gate "
+                             f"{int(ids[k])} reads wire {w} defined later")
+    lv = _levels_native(pos)
+    if lv is not None:
+        return lv
+    lv = np.zeros(len(ids), dtype=np.int64)
     for k in range(len(ids)):
         m = -1
-        for w in opnd[k]:
-            if w < 0:
-                continue
-            p = pos_of_wire[w]
-            if p >= k:
-                raise SchedulerError(
-                    "circuit is not a valid sequential form: gate "
-                    f"{int(ids[k])} reads wire {int(w)} defined later")
-            if p >= 0 and level_of_wire[w] > m:
-                m = level_of_wire[w]
+        for p in pos[k]:
+            if p >= 0 and lv[p] > m:
+                m = lv[p]
         lv[k] = m + 1
-        level_of_wire[ids[k]] = lv[k]
     return lv
 
 
@@ -139,17 +166,39 @@ def split_batches(groups: Mapping[GateKind, Sequence[int]], workers: int) -> lis
 
 
 def build_schedule(c: Circuit, workers: int) -> Schedule:
+    """Waves -> opcode groups in first-seen order -> <= `workers` contiguous
+    slices per group (scheduler.py:170-178), vectorised over the circuit arrays."""
     if workers < 1:
         raise SchedulerError(f"worker count must be >= 1, got {workers}")
-    waves = partition_waves(c)
-    by_id = {g.id: g for g in c.gates}
-    out = []
-    for wg in waves.order:
-        groups: dict[GateKind, list[int]] = {}
-        for gid in wg:
-            groups.setdefault(as_kind(by_id[gid].opcode), []).append(gid)
-        out.append(tuple(split_batches(groups, workers)))
-    return Schedule(waves=tuple(out), workers=workers)
+    ids, codes, _, _ = circuit_arrays(c)
+    G = len(ids)
+    if G == 0:
+        return Schedule(waves=(), workers=workers)
+    lv = wave_index(c)
+    depth = int(lv.max()) + 1
+    nk = len(_KINDS)
+    key = lv * nk + codes
+    first = np.full(depth * nk, G, dtype=np.int64)
+    np.minimum.at(first, key, np.arange(G, dtype=np.int64))
+    # stable order: wave, then the opcode's first appearance in the wave, then position
+    order = np.lexsort((np.arange(G), first[key], lv))
+    ks = key[order]
+    starts = np.concatenate(([0], np.flatnonzero(np.diff(ks)) + 1, [G]))
+    gid_sorted = ids[order]
+    waves: list[list[Batch]] = [[] for _ in range(depth)]
+    for a, b in zip(starts[:-1].tolist(), starts[1:].tolist()):
+        w, op = divmod(int(ks[a]), nk)
+        m = b - a
+        q, r = divmod(m, workers)
+        s0 = a
+        for wk in range(workers):
+            size = q + (1 if wk < r else 0)
+            if size == 0:
+                break
+            waves[w].append(Batch(opcode=_KINDS[op], gate_ids=tuple(gid_sorted[s0:s0 + size].tolist()),
+                                  worker=wk))
+            s0 += size
+    return Schedule(waves=tuple(tuple(w) for w in waves), workers=workers)
 
 
 def bootstraps_of(schedule: Schedule) -> int:
