@@ -378,10 +378,10 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
         const uint32_t* from_partner = xg + (size_t)lv * (P / 2) * 32;
         uint32_t mine[P];
         const uint32_t idxh = idx0 + (uint32_t)(hh * M);
-  #pragma unroll
+#pragma unroll
         for (int m1 = 0; m1 < P; m1 += 2) {
           uint32_t oth[2];
-  #pragma unroll
+#pragma unroll
           for (int q = 0; q < 2; ++q) {
             const uint32_t idx = (idxh + (uint32_t)(L * (m1 + q))) & two_n_mask;
             const uint32_t v = A[idx & (N - 1)];
@@ -393,10 +393,10 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
           to_partner[(m1 / 2) * 32 + lane] = oth[0] | (oth[1] << 16);
         }
         named_barrier(5 + 2 * gl + cr, 64);
-  #pragma unroll
+#pragma unroll
         for (int m1 = 0; m1 < P; m1 += 2) {
           const uint32_t w = from_partner[(m1 / 2) * 32 + lane];
-  #pragma unroll
+#pragma unroll
           for (int q = 0; q < 2; ++q) {
             const uint32_t rv = q ? (w >> 16) : (w & 0xFFFFu);
             const uint32_t re = hh ? rv : mine[m1 + q], im = hh ? mine[m1 + q] : rv;
