@@ -67,6 +67,18 @@ def test_config1_first_gates_p128(engine_mod, golden_p128, p128_keys):
     assert np.array_equal(acc, golden_p128["acc2"])
 
 
+def test_first_gates_p110(engine_mod, golden_p110, p110_keys):
+    """PARAM_110 (n = 512): the reference's own accumulators and NAND outputs."""
+    from paper_2306_11006_b200.cggi import PARAM_110, GateKind, eval_gate_batch
+    ek = p110_keys.eval_key()
+    tv = np.zeros((2, PARAM_110.N), np.uint32)
+    tv[1, :] = PARAM_110.mu
+    acc = ek.engine().blind_rotate(golden_p110["lin2"], tv)
+    assert np.array_equal(acc, golden_p110["acc2"])
+    out = eval_gate_batch(GateKind.NAND, [golden_p110["in_a_head"], golden_p110["in_b_head"]], ek)
+    assert np.array_equal(out, golden_p110["out_head"])
+
+
 def test_config1_digest_p128(engine_mod, golden_json, golden_p128, p128_keys):
     """256 NAND bootstraps, output sha256[:16] 6b796965e2579b67."""
     from paper_2306_11006_b200.cggi import PARAM_128, GateKind, OpCounter, decrypt_rows, \
