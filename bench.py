@@ -348,7 +348,7 @@ def run_ours(args):
     # the kernel the engine launches for this batch (gw_api.cu launch_v3: gates per CTA
     # minimising waves x measured step time; loader-warp key streaming below 4 per CTA)
     sms = torch.cuda.get_device_properties(local).multi_processor_count
-    step_kcyc = {1: 7.8, 2: 9.6, 3: 12.8, 4: 17.7}   # gw_api.cu launch_v3 policy
+    step_kcyc = {1: 7.8, 2: 9.6, 3: 12.6, 4: 17.7}   # gw_api.cu launch_v3 policy
     gc = min(step_kcyc, key=lambda g: (-(-G // (sms * g)) * step_kcyc[g], g))
     kname = f"k_blind_rotate_v3<{gc},{0 if gc == 4 else 2}>"
     traffic = None

@@ -145,7 +145,8 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
   uint64_t* full_bar = bars;       // [2] every warp stored its share of the slab in TMEM buffer b
   uint64_t* empty_bar = bars + 2;  // [2] every warp finished its MAC reads of buffer b
   uint64_t* stage_bar = bars + 4;  // TMA mode: slab landed in shared memory
-  uint32_t* tm_slot = reinterpret_cast<uint32_t*>(bars + 6);
+  uint64_t* go_bar = bars + 5;     // [2] stagger (GC = 3): gate 0 finished F(0) / M(0)
+  uint32_t* tm_slot = reinterpret_cast<uint32_t*>(bars + 7);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, l = lane;
   const int gl = warp >> 2, o = warp & 3;
@@ -161,6 +162,8 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
       mbar_init(&empty_bar[k], 4 * GC);
     }
     mbar_init(stage_bar, 1);
+    mbar_init(&go_bar[0], 4);
+    mbar_init(&go_bar[1], 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) tm_alloc(tm_slot, 512);
@@ -350,6 +353,10 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
     }
   } else {
   if constexpr (LDR && GC >= 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(CREG));
+  // Stagger (GC = 3, measured +1 %): gate 1 starts once gate 0 has finished F(0),
+  // gate 2 once it has finished M(0), so the gates run different phases at once.
+  constexpr bool kStagger = LDR && GC == 3;
+  if (kStagger && gl >= 1) mbar_wait(&go_bar[gl - 1], 0);
   uint32_t a_next = __ldg(lin_g);
   for (int i = 0; i < a.n; ++i) {
     const int cur = i & 1, nxt = cur ^ 1;
@@ -444,6 +451,7 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
 #pragma unroll
       for (int c = 0; c < P; ++c) tile[c * L + pos] = x[c];
     }
+    if (kStagger && i == 0 && gl == 0 && lane == 0) mbar_arrive(&go_bar[0]);
     mark(0);
     if (KM == 0 && pre) {  // buffer nxt is free once every warp finished MAC(i-1)
       if (i >= 1) mbar_wait(&empty_bar[nxt], (uint32_t)(((i - 1) >> 1) & 1));
@@ -498,6 +506,7 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
       }
     }
     release(&empty_bar[cur]);
+    if (kStagger && i == 0 && gl == 0 && lane == 0) mbar_arrive(&go_bar[1]);
     mark(2);
     if (pre) {
       kstore(i, sn, 1);
