@@ -371,6 +371,29 @@ def run_ours(args):
                 "peak_source": "measured DFMA peak, tools/microbench/pipes.cu "
                                "(profiles/r01_microbench_pipes.txt); not in MEASURED_PEAKS.json"}
 
+    # ---- informational: a wide level (12 x 148 gates, 3 per SM, 4 waves) -----
+    wide = None
+    if not args.no_netlist:
+        Gw = 12 * torch.cuda.get_device_properties(local).multi_processor_count
+        rng_w = np.random.default_rng(4242 + rank)
+        opsw = torch.from_numpy(rng_w.integers(0, 2 ** 32, (2 * Gw, Wp), dtype=np.uint32).view(np.int32)).cuda()
+        outw = torch.zeros((Gw, Wp), dtype=torch.int32, device="cuda")
+        pw, qw = opsw.data_ptr(), opsw.data_ptr() + Gw * Wp * 4
+        for _ in range(2):
+            eng.eval_gate_batch_device(nand, [pw, qw], Wp, Gw, outw.data_ptr(), Wp)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(3):
+            eng.eval_gate_batch_device(nand, [pw, qw], Wp, Gw, outw.data_ptr(), Wp)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wms = e0.elapsed_time(e1) / 3
+        wide = {"gates": Gw, "ms": wms, "gates_per_s": Gw / (wms / 1e3),
+                "fp64_frac": 157_409_280 * Gw / (wms / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
+                "note": "device-resident NAND batch, 3 gates per SM (the netlists' wide levels)"}
+        del opsw, outw
+
     # ---- end to end through the public API (pinned host buffers) ----------
     pa_h = torch.from_numpy(A.view(np.int32)).pin_memory().numpy().view(np.uint32)
     pb_h = torch.from_numpy(B.view(np.int32)).pin_memory().numpy().view(np.uint32)
@@ -422,6 +445,7 @@ def run_ours(args):
             "roofline": roofline,
             "cpu_baseline": cpu,
             "app_latency_config2": netlist,
+            "throughput_wide_level": wide,
             "clocks": clk.summary(),
             "parity": parity,
         }
