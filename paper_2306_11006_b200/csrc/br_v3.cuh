@@ -281,7 +281,11 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
       acc_g[o * N + j] = m < (uint32_t)N ? tvc[m] : 0u - tvc[m - N];
     }
   }
+  // orders the twiddle-table tcgen05.st (and the prologue key stores) before
+  // every warp's tcgen05.ld
+  tm_fence_before();
   __syncthreads();
+  tm_fence_after();
 
   // MAC-phase geometry of this lane: pairs (k1, c_p), p = 0, 1
   const int mk1 = lane & 15;
