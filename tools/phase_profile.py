@@ -18,7 +18,7 @@ tv[1] = PARAM_128.mu
 eng.blind_rotate(lin, tv)
 eng.blind_rotate(lin, tv)
 cyc = eng.br_phase_cycles()
-names = ["forward", "fill S1", "barrier A", "MAC", "inverse", "S3+step barrier"]
+names = ["F", "wait B1", "M", "wait B2", "I", "wait B3"]  # br_v3.cuh phase marks
 tot = sum(cyc[0])
 print(f"gates={gates}: cycles per step (warp o of gate 0), total {tot / PARAM_128.n:.0f}")
 for w in range(4):
