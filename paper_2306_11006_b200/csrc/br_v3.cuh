@@ -1,9 +1,10 @@
 // br_v3.cuh -- blind rotation v3: frequency-partitioned MAC, bootstrapping key
-// streamed L2 -> registers -> double-buffered TMEM.
+// streamed L2 -> registers -> a TMEM ring, lane twiddles resident in TMEM.
 // Reference: gatewave/cggi.py:592-667 (`_blind_rotate_kernel`), PARAM_128 /
 // PARAM_110 geometry (N = 1024, l = 2: four gadget rows, four MAC outputs).
 //
-// CTA = GC gates x 4 warps, one CTA per SM (it owns all 512 TMEM columns).
+// CTA = GC gates x 4 compute warps (+ 4 key-loader warps for GC <= 3), one
+// CTA per SM (it owns all 512 TMEM columns).
 // Per step i, per gate:
 //   F  warp r (row r = (component r/2, level r%2)): rotate-subtract +
 //      gadget-decompose acc[r/2] (cggi.py:627-644), fold + twist, forward FFT
@@ -18,14 +19,9 @@
 //      (cggi.py:658-666; wrap-around adds commute, so the result is exact).
 // Compared to v2 (br_tmem.cuh), every shared-memory value is read once per
 // step instead of four times, and the lane-pair radix-2 stage needs no
-// shuffles or selects.  The key slab of step i+1 (128 KB: 64 complex per TMEM
-// lane) goes into the idle TMEM buffer either by the warps themselves (LDG
-// mode, GC >= 2: coalesced 16-byte loads issued at the phase boundaries of
-// step i, tcgen05.st) or, where 128 KB of shared memory is spare (GC = 1), by
-// one thread: cp.async.bulk L2 -> shared memory, tcgen05.cp -> TMEM.
-// Staging through shared memory costs 256 KB of shared-memory traffic per SM
-// and step, which the GC >= 2 configurations cannot afford (measured,
-// DESIGN.md §4).
+// shuffles or selects.  The key slab of a step (128 KB: 64 complex per TMEM
+// lane, four 64-column chunks) lives in a 7-chunk TMEM ring next to the lane
+// twiddle table (64 columns); see the KM modes below for who fills it.
 #pragma once
 #include "blind_rotate.cuh"
 #include "ks_tc.cuh"
@@ -101,12 +97,16 @@ __device__ __forceinline__ void tm_cp_128x256b(uint32_t taddr, uint64_t desc) {
   asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(desc) : "memory");
 }
 
-// Key streaming modes.  LDG (GC >= 2): every warp loads its share of the next
-// slab with 16-byte global loads at the four phase points of a step and stores
-// it into the idle TMEM buffer (tcgen05.st.32x32b.x4 straight from the load
-// registers).  TMA (GC = 1, where 128 KB of shared memory is spare): warp 0
-// copies the slab L2 -> shared memory (cp.async.bulk) -> TMEM (tcgen05.cp),
-// so no compute warp spends registers or issue slots on the key.
+// Key streaming modes (KM).  2, the default for GC <= 3: four loader warps
+// (one per TMEM sub-partition) load each slab with 16-24 coalesced 16-byte
+// loads in flight and store it with tcgen05.st, up to two steps ahead (chunks
+// 0-2 of slab i wait for MAC(i-2), chunk 3 for MAC(i-1)); at GC = 2, 3
+// setmaxnreg gives the compute warps CREG and the loaders LREG registers.
+// 0 (GC = 4, or GATEWAVE_BR_LDR=0): the compute warps load their share at the
+// four phase points of a step.  1 (GC = 1 with GATEWAVE_BR_GC1=tma): warp 0
+// stages the slab through shared memory (cp.async.bulk -> tcgen05.cp), which
+// costs 256 KB of shared-memory traffic per step (measured slower).
+//
 // digit extraction shared by the two level-warps of a component (one extraction
 // + a shared-memory swap + a pair barrier) or done by every row warp alone
 constexpr bool kShareDigits = true;  // measured: sharing is 2-5 % faster
@@ -124,9 +124,7 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
   using G = V3::G;
   constexpr int N = V3::N, M = V3::M, P = V3::P, L = V3::L, R = V3::R, LEV = V3::LEV, LOGN = V3::LOGN;
   constexpr int UB = V3::UB, COLS = V3::COLS, CIDX = V3::CIDX;
-  // key streaming: warp (gl, w) fills cidx [gl*KPW, (gl+1)*KPW) of sub-partition w,
-  // 8 complex (32 columns, one tcgen05.st) per group, GPP groups per phase point
-  // LDG mode: the slab is 8 groups of 8 cidx; warp (gl, w) owns groups gl, gl+GC, ...
+  // KM = 0: the slab is 8 groups of 8 cidx; warp (gl, w) owns groups gl, gl+GC, ...
   // and handles group list entry j at phase point j % 4 (GC = 1: two per point)
   constexpr int NG = (8 + GC - 1) / GC;     // max groups per warp
   constexpr int GPP = (NG + 3) / 4;         // groups per phase point
