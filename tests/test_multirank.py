@@ -75,19 +75,20 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_two_rank_exchange_matches_plaintext():
+@pytest.mark.parametrize("world", [2, 3])
+def test_multi_rank_exchange_matches_plaintext(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=180) for _ in procs)
     for p in procs:
         p.join(timeout=60)
-    for rank in (0, 1):
+    for rank in range(world):
         for ok, gpus, _ in res[rank]:
-            assert ok and gpus == 2
+            assert ok and gpus == world
 
 
 def test_exchange_plan_moves_only_cross_rank_wires():
