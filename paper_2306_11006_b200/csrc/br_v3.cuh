@@ -107,10 +107,6 @@ __device__ __forceinline__ void tm_cp_128x256b(uint32_t taddr, uint64_t desc) {
 // stages the slab through shared memory (cp.async.bulk -> tcgen05.cp), which
 // costs 256 KB of shared-memory traffic per step (measured slower).
 //
-// digit extraction shared by the two level-warps of a component (one extraction
-// + a shared-memory swap + a pair barrier) or done by every row warp alone
-constexpr bool kShareDigits = true;  // measured: sharing is 2-5 % faster
-
 // KM = key streaming mode: 0 LDG by the compute warps, 1 TMA by warp 0, 2 four
 // dedicated loader warps (one per TMEM sub-partition; GC = 1 only).
 template <int GC, int KM>
@@ -376,67 +372,41 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
       const uint32_t abar = ((a_i + radd) >> rshift) & two_n_mask;
       const uint32_t idx0 = ((uint32_t)l - abar) & two_n_mask;
       double2 x[P];
-      if constexpr (kShareDigits) {
-        // The two level-warps of component cr split the coefficients by half
-        // (warp lv takes j + lv*M), extract BOTH digit levels of their half and
-        // swap the other level's digits through shared memory.
-        const int hh = lv;
-        const int sh_mine = 32 - (lv + 1) * a.bg_bits, sh_other = 32 - (2 - lv) * a.bg_bits;
-        uint32_t* xg = xchg_all + (size_t)gl * V3::XCHG + (size_t)cr * 2 * (P / 2) * 32;
-        uint32_t* to_partner = xg + (size_t)(1 - lv) * (P / 2) * 32;
-        const uint32_t* from_partner = xg + (size_t)lv * (P / 2) * 32;
-        uint32_t mine[P];
-        const uint32_t idxh = idx0 + (uint32_t)(hh * M);
+      // The two level-warps of component cr split the coefficients by half
+      // (warp lv takes j + lv*M), extract BOTH digit levels of their half and
+      // swap the other level's digits through shared memory.
+      const int hh = lv;
+      const int sh_mine = 32 - (lv + 1) * a.bg_bits, sh_other = 32 - (2 - lv) * a.bg_bits;
+      uint32_t* xg = xchg_all + (size_t)gl * V3::XCHG + (size_t)cr * 2 * (P / 2) * 32;
+      uint32_t* to_partner = xg + (size_t)(1 - lv) * (P / 2) * 32;
+      const uint32_t* from_partner = xg + (size_t)lv * (P / 2) * 32;
+      uint32_t mine[P];
+      const uint32_t idxh = idx0 + (uint32_t)(hh * M);
 #pragma unroll
-        for (int m1 = 0; m1 < P; m1 += 2) {
-          uint32_t oth[2];
+      for (int m1 = 0; m1 < P; m1 += 2) {
+        uint32_t oth[2];
 #pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const uint32_t idx = (idxh + (uint32_t)(L * (m1 + q))) & two_n_mask;
-            const uint32_t v = A[idx & (N - 1)];
-            const uint32_t neg = 0u - ((idx >> LOGN) & 1u);  // all ones past X^N
-            const uint32_t buf = ((v ^ neg) - neg) - A[L * (m1 + q) + l + hh * M] + a.offs;
-            mine[m1 + q] = (buf >> sh_mine) & base_mask;
-            oth[q] = (buf >> sh_other) & base_mask;
-          }
-          to_partner[(m1 / 2) * 32 + lane] = oth[0] | (oth[1] << 16);
+        for (int q = 0; q < 2; ++q) {
+          const uint32_t idx = (idxh + (uint32_t)(L * (m1 + q))) & two_n_mask;
+          const uint32_t v = A[idx & (N - 1)];
+          const uint32_t neg = 0u - ((idx >> LOGN) & 1u);  // all ones past X^N
+          const uint32_t buf = ((v ^ neg) - neg) - A[L * (m1 + q) + l + hh * M] + a.offs;
+          mine[m1 + q] = (buf >> sh_mine) & base_mask;
+          oth[q] = (buf >> sh_other) & base_mask;
         }
-        named_barrier(5 + 2 * gl + cr, 64);
+        to_partner[(m1 / 2) * 32 + lane] = oth[0] | (oth[1] << 16);
+      }
+      named_barrier(5 + 2 * gl + cr, 64);
 #pragma unroll
-        for (int m1 = 0; m1 < P; m1 += 2) {
-          const uint32_t w = from_partner[(m1 / 2) * 32 + lane];
+      for (int m1 = 0; m1 < P; m1 += 2) {
+        const uint32_t w = from_partner[(m1 / 2) * 32 + lane];
 #pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const uint32_t rv = q ? (w >> 16) : (w & 0xFFFFu);
-            const uint32_t re = hh ? rv : mine[m1 + q], im = hh ? mine[m1 + q] : rv;
-            double2 v = make_double2(digit_to_double_lo(re, dmagic), digit_to_double_lo(im, dmagic));
-            if (m1 + q > 0) v = cmul(v, c_root64[G::CSTEP * (m1 + q)]);
-            x[bitrev_c<G::LOGP>(m1 + q)] = v;  // DIT forward takes bit-reversed input
-          }
-        }
-      } else {
-        // every row warp extracts its own digit level from all its coefficients
-        const int sh = 32 - (lv + 1) * a.bg_bits;
-        uint32_t vr[2 * P], va[2 * P];
-#pragma unroll
-        for (int k = 0; k < 2 * P; ++k) {  // k = 2*m1 + hh: coefficient j = L*m1 + l + hh*M
-          const int m1 = k >> 1, hh = k & 1;
-          vr[k] = A[((idx0 + (uint32_t)(L * m1 + hh * M)) & two_n_mask) & (N - 1)];
-          va[k] = A[L * m1 + l + hh * M];
-        }
-#pragma unroll
-        for (int m1 = 0; m1 < P; ++m1) {
-          double dd[2];
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            const uint32_t idx = (idx0 + (uint32_t)(L * m1 + hh * M)) & two_n_mask;
-            const uint32_t neg = 0u - ((idx >> LOGN) & 1u);  // all ones past X^N
-            const uint32_t buf = ((vr[2 * m1 + hh] ^ neg) - neg) - va[2 * m1 + hh] + a.offs;
-            dd[hh] = digit_to_double_lo((buf >> sh) & base_mask, dmagic);
-          }
-          double2 v = make_double2(dd[0], dd[1]);
-          if (m1 > 0) v = cmul(v, c_root64[G::CSTEP * m1]);
-          x[bitrev_c<G::LOGP>(m1)] = v;
+        for (int q = 0; q < 2; ++q) {
+          const uint32_t rv = q ? (w >> 16) : (w & 0xFFFFu);
+          const uint32_t re = hh ? rv : mine[m1 + q], im = hh ? mine[m1 + q] : rv;
+          double2 v = make_double2(digit_to_double_lo(re, dmagic), digit_to_double_lo(im, dmagic));
+          if (m1 + q > 0) v = cmul(v, c_root64[G::CSTEP * (m1 + q)]);
+          x[bitrev_c<G::LOGP>(m1 + q)] = v;  // DIT forward takes bit-reversed input
         }
       }
       double2* tile = U + (size_t)o * P * L;
