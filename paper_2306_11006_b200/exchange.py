@@ -19,7 +19,7 @@ import numpy as np
 
 from .cggi import EvalKey
 from .circuit import Circuit
-from .runtime import EvaluateError, Metrics, compile_plan
+from .runtime import EvaluateError, Metrics
 from .scheduler import Schedule
 
 

@@ -21,7 +21,7 @@ def _worker(rank, world, port, q):
     torch.cuda.set_device(0)
     from paper_2306_11006_b200 import circuit as C
     from paper_2306_11006_b200 import netlists as NL
-    from paper_2306_11006_b200.cggi import EvalKey, encrypt_bits, keygen
+    from paper_2306_11006_b200.cggi import encrypt_bits, keygen
     from paper_2306_11006_b200.rng import SeededRng
     from paper_2306_11006_b200.runtime import evaluate
     from paper_2306_11006_b200.scheduler import build_schedule

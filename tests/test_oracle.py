@@ -4,7 +4,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from conftest import MINI, digest
+from conftest import MINI
 
 
 def test_ntt_matches_reference_mini(golden_mini):
