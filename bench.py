@@ -394,6 +394,37 @@ def run_ours(args):
                 "note": "device-resident NAND batch, 3 gates per SM (the netlists' wide levels)"}
         del opsw, outw
 
+    # ---- informational: the secondary parameter set (PARAM_110, n = 512) ----
+    p110 = None
+    if not args.no_netlist:
+        from paper_2306_11006_b200.cggi import PARAM_110
+        ks110, A110, B110, a110, b110 = _workload(PARAM_110, rank, G)
+        ek110 = ks110.eval_key()
+        e110 = ek110.engine()
+        e110.set_stream(stream.cuda_stream)
+        W1 = PARAM_110.n + 1
+        Wp1 = (W1 + 3) & ~3
+        ops1 = torch.zeros((2 * G, Wp1), dtype=torch.int32, device="cuda")
+        ops1[:G, :W1] = torch.from_numpy(A110.view(np.int32))
+        ops1[G:, :W1] = torch.from_numpy(B110.view(np.int32))
+        out1 = torch.zeros((G, Wp1), dtype=torch.int32, device="cuda")
+        q0, q1 = ops1.data_ptr(), ops1.data_ptr() + G * Wp1 * 4
+        for _ in range(2):
+            e110.eval_gate_batch_device(nand, [q0, q1], Wp1, G, out1.data_ptr(), Wp1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(5):
+            e110.eval_gate_batch_device(nand, [q0, q1], Wp1, G, out1.data_ptr(), Wp1)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        pms = e0.elapsed_time(e1) / 5
+        ok110 = bool(np.array_equal(decrypt_rows(ks110.lwe_sk, out1[:, :W1].cpu().numpy().view(np.uint32)),
+                                    (1 - (a110 & b110)).astype(np.uint8)))
+        p110 = {"params": "PARAM_110 (n=512)", "gates": G, "ms": pms, "gates_per_s": G / (pms / 1e3),
+                "decrypt_ok": ok110}
+        del ops1, out1
+
     # ---- end to end through the public API (pinned host buffers) ----------
     pa_h = torch.from_numpy(A.view(np.int32)).pin_memory().numpy().view(np.uint32)
     pb_h = torch.from_numpy(B.view(np.int32)).pin_memory().numpy().view(np.uint32)
@@ -446,6 +477,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "app_latency_config2": netlist,
             "throughput_wide_level": wide,
+            "param110": p110,
             "clocks": clk.summary(),
             "parity": parity,
         }
