@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
   uint64_t* full_bar = bars;       // [2] every warp stored its share of the slab in TMEM buffer b
   uint64_t* empty_bar = bars + 2;  // [2] every warp finished its MAC reads of buffer b
   uint64_t* stage_bar = bars + 4;  // TMA mode: slab landed in shared memory
-  uint64_t* go_bar = bars + 5;     // [2] stagger (GC = 3): gate 0 finished F(0) / M(0)
+  uint64_t* go_bar = bars + 5;     // [2] stagger: gate 0 reached its start points for gates 1 / 2
   uint32_t* tm_slot = reinterpret_cast<uint32_t*>(bars + 7);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, l = lane;
@@ -351,9 +351,11 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
     }
   } else {
   if constexpr (LDR && GC >= 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(CREG));
-  // Stagger (GC = 3, measured +1 %): gate 1 starts once gate 0 has finished F(0),
-  // gate 2 once it has finished M(0), so the gates run different phases at once.
-  constexpr bool kStagger = LDR && GC == 3;
+  // Stagger (measured: GC = 3 +1 %, GC = 2 +0-7 %): the gates of a CTA start at
+  // different points of step 0 so they run different phases at once.  GC = 3:
+  // gate 1 after gate 0's F(0), gate 2 after its M(0); GC = 2: gate 1 after gate
+  // 0's digit decomposition (its integer work then overlaps gate 0's FFTs).
+  constexpr bool kStagger = LDR && (GC == 3 || GC == 2);
   if (kStagger && gl >= 1) mbar_wait(&go_bar[gl - 1], 0);
   uint32_t a_next = __ldg(lin_g);
   for (int i = 0; i < a.n; ++i) {
@@ -409,6 +411,7 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
           x[bitrev_c<G::LOGP>(m1 + q)] = v;  // DIT forward takes bit-reversed input
         }
       }
+      if (GC == 2 && kStagger && i == 0 && gl == 0 && lane == 0) mbar_arrive(&go_bar[0]);
       double2* tile = U + (size_t)o * P * L;
       if constexpr (GC <= 2) {
         double2 tw[P];
@@ -423,7 +426,7 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
 #pragma unroll
       for (int c = 0; c < P; ++c) tile[c * L + pos] = x[c];
     }
-    if (kStagger && i == 0 && gl == 0 && lane == 0) mbar_arrive(&go_bar[0]);
+    if (GC == 3 && kStagger && i == 0 && gl == 0 && lane == 0) mbar_arrive(&go_bar[0]);
     mark(0);
     if (KM == 0 && pre) {  // buffer nxt is free once every warp finished MAC(i-1)
       if (i >= 1) mbar_wait(&empty_bar[nxt], (uint32_t)(((i - 1) >> 1) & 1));
