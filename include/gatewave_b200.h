@@ -124,6 +124,25 @@ int gw_plan_run(gw_ctx* ctx, gw_plan* plan);
 int gw_plan_run_levels(gw_ctx* ctx, gw_plan* plan, int64_t first, int64_t last);
 int gw_plan_destroy(gw_ctx* ctx, gw_plan* plan);
 
+/* Multi-GPU wire exchange between levels (replaces the reference's per-wave
+ * WireStore hand-off, runtime.py:166-190, for one process per GPU; SURVEY.md
+ * §8(b) gw_exchange_enqueue).  The static plan lists, per level and rank, the
+ * wire ids that rank produces and another rank reads later (or that are
+ * circuit outputs): ids[offsets[level*world + q] .. offsets[level*world + q + 1]).
+ * pack copies this rank's rows of a level into a contiguous device buffer of
+ * `pad` rows (the per-level maximum, gw_xplan_pad); the caller's collective
+ * (an all-gather over NCCL / NVLink) produces world x pad rows; unpack
+ * scatters the other ranks' rows into the wire store.  Both only enqueue on
+ * the context stream, so levels, exchanges and the collective stay
+ * stream-ordered with no host synchronisation. */
+typedef struct gw_xplan gw_xplan;
+int gw_xplan_create(gw_ctx* ctx, int64_t n_levels, int32_t world, const int64_t* offsets, const int64_t* ids,
+                    gw_xplan** out);
+int gw_xplan_pad(gw_ctx* ctx, const gw_xplan* plan, int64_t level, int64_t* pad);
+int gw_exchange_pack(gw_ctx* ctx, const gw_xplan* plan, int64_t level, int32_t rank, uint32_t* d_send);
+int gw_exchange_unpack(gw_ctx* ctx, const gw_xplan* plan, int64_t level, int32_t rank, const uint32_t* d_recv);
+int gw_xplan_destroy(gw_ctx* ctx, gw_xplan* plan);
+
 /* CUDA-event timer on the context stream (milliseconds between start/stop). */
 int gw_timer_start(gw_ctx* ctx);
 int gw_timer_stop(gw_ctx* ctx, float* ms);

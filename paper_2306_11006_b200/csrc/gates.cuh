@@ -43,6 +43,27 @@ __global__ void k_lin(const uint32_t* __restrict__ rows, int64_t stride, const L
   }
 }
 
+// Wire exchange: rows of a level's send list <-> a contiguous buffer (uint4 moves).
+__global__ void k_xpack(const uint32_t* __restrict__ wires, int64_t stride, const int64_t* __restrict__ ids,
+                        int64_t count, uint32_t* __restrict__ dst, int64_t dst_stride) {
+  const int64_t row = blockIdx.y;
+  if (row >= count) return;
+  const uint4* s4 = reinterpret_cast<const uint4*>(wires + (size_t)ids[row] * stride);
+  uint4* d4 = reinterpret_cast<uint4*>(dst + (size_t)row * dst_stride);
+  for (int k = threadIdx.x; k < stride / 4; k += blockDim.x) d4[k] = s4[k];
+}
+__global__ void k_xunpack(uint32_t* __restrict__ wires, int64_t stride, const int64_t* __restrict__ ids,
+                          const int64_t* __restrict__ offs, int world, int rank, int64_t pad,
+                          const uint32_t* __restrict__ recv) {
+  const int q = blockIdx.z, row = blockIdx.y;
+  if (q == rank) return;
+  const int64_t n = offs[q + 1] - offs[q];
+  if (row >= n) return;
+  const uint4* s4 = reinterpret_cast<const uint4*>(recv + ((size_t)q * pad + row) * stride);
+  uint4* d4 = reinterpret_cast<uint4*>(wires + (size_t)ids[offs[q] + row] * stride);
+  for (int k = threadIdx.x; k < stride / 4; k += blockDim.x) d4[k] = s4[k];
+}
+
 __global__ void k_zero_units(const KsUnit* __restrict__ units, int U, uint32_t* out, int64_t stride, int W) {
   const int u = blockIdx.y;
   if (u >= U) return;

@@ -1210,6 +1210,91 @@ int gw_plan_destroy(gw_ctx* c, gw_plan* p) {
   return GW_OK;
 }
 
+struct gw_xplan {
+  int64_t n_levels = 0;
+  int world = 1;
+  std::vector<int64_t> offs;  // host copy: (n_levels * world + 1)
+  std::vector<int64_t> pad;   // per level: max rows any rank sends
+  int64_t* d_offs = nullptr;  // device copy of offs
+  int64_t* d_ids = nullptr;
+};
+
+int gw_xplan_create(gw_ctx* c, int64_t n_levels, int32_t world, const int64_t* offsets, const int64_t* ids,
+                    gw_xplan** out) {
+  if (!c || !out || n_levels < 0 || world < 1 || (n_levels > 0 && !offsets)) return GW_ERR_ARG;
+  *out = nullptr;
+  const int64_t nl = n_levels * world;
+  if (offsets[0] != 0) return fail(c, GW_ERR_ARG, "exchange offsets must start at 0");
+  for (int64_t k = 0; k < nl; ++k)
+    if (offsets[k + 1] < offsets[k]) return fail(c, GW_ERR_ARG, "exchange offsets must not decrease");
+  const int64_t total = offsets[nl];
+  if (total > 0 && !ids) return GW_ERR_ARG;
+  for (int64_t k = 0; k < total; ++k)
+    if (ids[k] < 0 || ids[k] >= c->wire_slots)
+      return fail(c, GW_ERR_WIRE, "exchange wire id out of range: " + std::to_string(ids[k]));
+  cudaSetDevice(c->device);
+  gw_xplan* x = new gw_xplan();
+  x->n_levels = n_levels;
+  x->world = world;
+  x->offs.assign(offsets, offsets + nl + 1);
+  x->pad.assign(n_levels, 0);
+  for (int64_t L = 0; L < n_levels; ++L)
+    for (int q = 0; q < world; ++q)
+      x->pad[L] = std::max<int64_t>(x->pad[L], offsets[L * world + q + 1] - offsets[L * world + q]);
+  cudaError_t e = cudaMalloc(&x->d_offs, (nl + 1) * sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaMemcpy(x->d_offs, offsets, (nl + 1) * sizeof(int64_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && total > 0) e = cudaMalloc(&x->d_ids, total * sizeof(int64_t));
+  if (e == cudaSuccess && total > 0) e = cudaMemcpy(x->d_ids, ids, total * sizeof(int64_t), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    gw_xplan_destroy(c, x);
+    return fail(c, GW_ERR_CUDA, cudaGetErrorString(e));
+  }
+  *out = x;
+  return GW_OK;
+}
+
+int gw_xplan_pad(gw_ctx* c, const gw_xplan* x, int64_t level, int64_t* pad) {
+  if (!c || !x || !pad || level < 0 || level >= x->n_levels) return GW_ERR_ARG;
+  *pad = x->pad[level];
+  return GW_OK;
+}
+
+int gw_exchange_pack(gw_ctx* c, const gw_xplan* x, int64_t level, int32_t rank, uint32_t* d_send) {
+  if (!c || !x || level < 0 || level >= x->n_levels || rank < 0 || rank >= x->world) return GW_ERR_ARG;
+  if (!c->wires) return fail(c, GW_ERR_STATE, "wire store not allocated");
+  const int64_t k0 = x->offs[level * x->world + rank], n = x->offs[level * x->world + rank + 1] - k0;
+  if (n == 0) return GW_OK;
+  if (!d_send) return GW_ERR_ARG;
+  cudaSetDevice(c->device);
+  dim3 grid(1, (unsigned)n);
+  k_xpack<<<grid, 160, 0, c->stream>>>(c->wires, c->Wp, x->d_ids + k0, n, d_send, c->Wp);
+  GW_LAUNCHED(c);
+  return GW_OK;
+}
+
+int gw_exchange_unpack(gw_ctx* c, const gw_xplan* x, int64_t level, int32_t rank, const uint32_t* d_recv) {
+  if (!c || !x || level < 0 || level >= x->n_levels || rank < 0 || rank >= x->world) return GW_ERR_ARG;
+  if (!c->wires) return fail(c, GW_ERR_STATE, "wire store not allocated");
+  const int64_t pad = x->pad[level];
+  if (pad == 0 || x->world == 1) return GW_OK;
+  if (!d_recv) return GW_ERR_ARG;
+  cudaSetDevice(c->device);
+  dim3 grid(1, (unsigned)pad, (unsigned)x->world);
+  k_xunpack<<<grid, 160, 0, c->stream>>>(c->wires, c->Wp, x->d_ids, x->d_offs + level * x->world, x->world, rank,
+                                          pad, d_recv);
+  GW_LAUNCHED(c);
+  return GW_OK;
+}
+
+int gw_xplan_destroy(gw_ctx* c, gw_xplan* x) {
+  if (!x) return GW_OK;
+  if (c) cudaSetDevice(c->device);
+  cudaFree(x->d_offs);
+  cudaFree(x->d_ids);
+  delete x;
+  return GW_OK;
+}
+
 int gw_timer_start(gw_ctx* c) {
   if (!c) return GW_ERR_ARG;
   GW_CUDA(c, cudaEventRecord(c->ev0, c->stream));

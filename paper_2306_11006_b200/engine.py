@@ -36,7 +36,8 @@ EXPORTS = ("gw_version", "gw_levels", "gw_device_count", "gw_create", "gw_destro
            "gw_eval_gate_batch_device", "gw_wires_alloc", "gw_wires_put", "gw_wires_get",
            "gw_wires_device_ptr", "gw_wires_attach", "gw_plan_create", "gw_plan_run", "gw_plan_run_levels",
            "gw_plan_destroy", "gw_timer_start", "gw_timer_stop", "gw_set_profiling",
-           "gw_stage_times", "gw_br_phase_cycles", "gw_launch_count")
+           "gw_stage_times", "gw_br_phase_cycles", "gw_launch_count", "gw_xplan_create", "gw_xplan_pad",
+           "gw_exchange_pack", "gw_exchange_unpack", "gw_xplan_destroy")
 
 
 class EngineUnavailable(RuntimeError):
@@ -99,6 +100,12 @@ def load_library(path: str | None = None):
             "gw_plan_run": ([_P, _P], ctypes.c_int),
             "gw_plan_run_levels": ([_P, _P, ctypes.c_int64, ctypes.c_int64], ctypes.c_int),
             "gw_plan_destroy": ([_P, _P], ctypes.c_int),
+            "gw_xplan_create": ([_P, ctypes.c_int64, ctypes.c_int32, _I64P, _I64P, ctypes.POINTER(_P)],
+                                ctypes.c_int),
+            "gw_xplan_pad": ([_P, _P, ctypes.c_int64, _I64P], ctypes.c_int),
+            "gw_exchange_pack": ([_P, _P, ctypes.c_int64, ctypes.c_int32, _P], ctypes.c_int),
+            "gw_exchange_unpack": ([_P, _P, ctypes.c_int64, ctypes.c_int32, _P], ctypes.c_int),
+            "gw_xplan_destroy": ([_P, _P], ctypes.c_int),
             "gw_timer_start": ([_P], ctypes.c_int),
             "gw_timer_stop": ([_P, ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
             "gw_set_profiling": ([_P, ctypes.c_int], ctypes.c_int),
@@ -325,6 +332,41 @@ class Engine:
             self._ctx, offs.shape[0] - 1, offs.ctypes.data_as(_I64P), ops.ctypes.data_as(_I32P),
             opnd.ctypes.data_as(_I32P), outs.ctypes.data_as(_I32P), ctypes.byref(h)))
         return Plan(self, h, offs.shape[0] - 1)
+
+
+class ExchangePlanHandle:
+    """Device-resident exchange plan (gw_xplan): pack / unpack one level's wires."""
+
+    def __init__(self, engine: "Engine", sends, world: int):
+        self.engine, self.world, self.n_levels = engine, world, len(sends)
+        offs, ids = [0], []
+        for lvl in sends:
+            for q in range(world):
+                a = np.asarray(lvl[q], dtype=np.int64)
+                ids.append(a)
+                offs.append(offs[-1] + a.shape[0])
+        self._offs = np.asarray(offs, dtype=np.int64)
+        self._ids = np.concatenate(ids) if ids else np.zeros(0, np.int64)
+        h = _P()
+        engine._check(engine._lib.gw_xplan_create(engine._ctx, self.n_levels, world, self._offs.ctypes.data_as(_I64P),
+                                                  self._ids.ctypes.data_as(_I64P), ctypes.byref(h)))
+        self._h = h
+
+    def pad(self, level: int) -> int:
+        v = ctypes.c_int64(0)
+        self.engine._check(self.engine._lib.gw_xplan_pad(self.engine._ctx, self._h, level, ctypes.byref(v)))
+        return v.value
+
+    def pack(self, level: int, rank: int, d_send: int):
+        self.engine._check(self.engine._lib.gw_exchange_pack(self.engine._ctx, self._h, level, rank, _P(d_send)))
+
+    def unpack(self, level: int, rank: int, d_recv: int):
+        self.engine._check(self.engine._lib.gw_exchange_unpack(self.engine._ctx, self._h, level, rank, _P(d_recv)))
+
+    def close(self):
+        if self._h:
+            self.engine._lib.gw_xplan_destroy(self.engine._ctx, self._h)
+            self._h = None
 
 
 class Plan:

@@ -99,7 +99,16 @@ class _DeviceLevels:
     def run_level(self, level: int):
         self.handle.run(level, level + 1)
 
+    def exchange_plan(self, sends, world: int):
+        """Device exchange plan: the level's send rows are packed / unpacked by
+        engine kernels on the engine stream (gw_exchange_pack / _unpack)."""
+        from .engine import ExchangePlanHandle
+        self.xplan = ExchangePlanHandle(self.eng, sends, world)
+        return self.xplan
+
     def close(self):
+        if getattr(self, "xplan", None) is not None:
+            self.xplan.close()
         self.handle.close()
         self.eng.wires_alloc(0)
 
@@ -146,6 +155,7 @@ def evaluate_distributed(c: Circuit, schedule: Schedule, mats: dict, ek: EvalKey
         lv = levels_factory(plan, slots, device)
     wires = lv.wires
     W = p.n + 1
+    dx = lv.exchange_plan(xplan.sends, world) if hasattr(lv, "exchange_plan") else None
     try:
         for port in c.inputs:
             ids = torch.as_tensor(np.asarray(port.wires, np.int64), device=device)
@@ -156,7 +166,12 @@ def evaluate_distributed(c: Circuit, schedule: Schedule, mats: dict, ek: EvalKey
             s = time.monotonic()
             lv.run_level(L)
             m = xplan.pad[L]
-            if m:
+            if m and dx is not None:   # engine kernels pack / unpack on the engine stream
+                send = torch.empty((m, wires.shape[1]), dtype=torch.int32, device=device)
+                dx.pack(L, rank, send.data_ptr())
+                recv = _all_gather(send, world, group)
+                dx.unpack(L, rank, recv.data_ptr())
+            elif m:                    # plaintext mock levels (CPU tests)
                 mine = xplan.sends[L][rank]
                 send = torch.zeros((m, wires.shape[1]), dtype=torch.int32, device=device)
                 if len(mine):

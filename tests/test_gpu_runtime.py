@@ -96,3 +96,34 @@ def test_evaluate_errors(mini_keys):
         evaluate(c, s, {"a": good, "b": np.zeros((2, MINI.n), np.uint32)}, mini_keys)
     with pytest.raises(EvaluateError):
         evaluate(c, build_schedule(C.gen_adder(3), 1), {"a": good, "b": good}, mini_keys)
+
+
+def test_exchange_pack_unpack_kernels(p128_keys):
+    """gw_exchange_pack / _unpack move exactly the planned wire rows."""
+    import torch
+    from paper_2306_11006_b200.cggi import PARAM_128
+    from paper_2306_11006_b200.engine import Engine, ExchangePlanHandle, params_tuple
+    eng = Engine(*params_tuple(PARAM_128), device=0)
+    slots, W = 64, PARAM_128.n + 1
+    eng.wires_alloc(slots)
+    rows = np.random.default_rng(5).integers(0, 2 ** 32, (slots, W), dtype=np.uint32)
+    eng.wires_put(np.arange(slots), rows)
+    sends = [[np.array([3, 7, 9]), np.array([20, 21])], [np.array([], np.int64), np.array([40])]]
+    x = ExchangePlanHandle(eng, sends, 2)
+    assert [x.pad(0), x.pad(1)] == [3, 1]
+    stride = eng.row_stride
+    send = torch.zeros((3, stride), dtype=torch.int32, device="cuda")
+    x.pack(0, 0, send.data_ptr())
+    torch.cuda.synchronize()
+    assert np.array_equal(send[:, :W].cpu().numpy().view(np.uint32), rows[[3, 7, 9]])
+    # rank 0 receives rank 1's rows of level 0 (wires 20, 21) from a fabricated all-gather
+    recv = torch.zeros((2 * 3, stride), dtype=torch.int32, device="cuda")
+    new = np.random.default_rng(6).integers(0, 2 ** 32, (2, W), dtype=np.uint32)
+    recv[3:5, :W] = torch.from_numpy(new.view(np.int32)).cuda()
+    x.unpack(0, 0, recv.data_ptr())
+    torch.cuda.synchronize()
+    got = eng.wires_get(np.arange(slots))
+    want = rows.copy()
+    want[[20, 21]] = new
+    assert np.array_equal(got, want)
+    x.close()
