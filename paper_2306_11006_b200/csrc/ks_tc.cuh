@@ -157,39 +157,45 @@ __global__ void __launch_bounds__(KT_THREADS, 1) k_keyswitch_tc(KtArgs a) {
     const uint32_t dmask = (1u << a.gamma) - 1;
     const uint32_t* urow = a.ut + (valid ? g : 0);
     // A K block spans KT_PAIRS / t input coefficients (t divides 32, so at most
-    // 32 when t = 1); the samples of block k+1 are loaded while block k is built,
-    // so the global-load latency overlaps the one-hot construction.
+    // 32 when t = 1).  The samples of the next PD - 1 blocks are in flight while
+    // block k is built (a register ring of PD blocks, PD * UMAX <= 32 words for
+    // t >= 2), so the global-load latency is paid once per PD blocks, not per block.
     constexpr int UMAX = KT_PAIRS / T;  // coefficients per K block
-    uint32_t ucur[UMAX], unext[UMAX];
+    constexpr int PD = T >= 2 ? T : 2;  // ring depth (blocks)
+    uint32_t ub[PD][UMAX];
     auto load_u = [&](int k, uint32_t (&dst)[UMAX]) {
       const int c0 = ((kb0 + k) * KT_PAIRS) / T;
 #pragma unroll
       for (int q = 0; q < UMAX; ++q)
         dst[q] = (valid && k < nkb) ? __ldg(urow + (size_t)(c0 + q) * a.ut_stride) : 0u;
     };
-    load_u(0, ucur);
-    for (int k = 0; k < nkb; ++k) {
-      const int s = k % KT_STAGES;
-      load_u(k + 1, unext);
-      mbar_wait(&empty[s], ((k / KT_STAGES) & 1) ^ 1);
-      uint8_t* dst = sA + (size_t)s * KT_A_BYTES + m * 16;
 #pragma unroll
-      for (int kc = 0; kc < KT_KB / 16; ++kc) {
-        uint32_t w[4];
+    for (int d = 0; d < PD; ++d) load_u(d, ub[d]);
+    for (int k0 = 0; k0 < nkb; k0 += PD) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int pl = kc * 4 + e;  // pair within the block; pairs of a coefficient are consecutive
-          const int j = pl % T;
-          const uint32_t u = ucur[pl / T];
-          const uint32_t d = (u >> ((T - 1 - j) * a.gamma)) & dmask;
-          w[e] = d ? (1u << (8 * (d - 1))) : 0u;
+      for (int d = 0; d < PD; ++d) {
+        const int k = k0 + d;
+        if (k >= nkb) break;
+        const int s = k % KT_STAGES;
+        mbar_wait(&empty[s], ((k / KT_STAGES) & 1) ^ 1);
+        uint8_t* dst = sA + (size_t)s * KT_A_BYTES + m * 16;
+#pragma unroll
+        for (int kc = 0; kc < KT_KB / 16; ++kc) {
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int pl = kc * 4 + e;  // pair within the block; pairs of a coefficient are consecutive
+            const int j = pl % T;
+            const uint32_t u = ub[d][pl / T];
+            const uint32_t dg = (u >> ((T - 1 - j) * a.gamma)) & dmask;
+            w[e] = dg ? (1u << (8 * (dg - 1))) : 0u;
+          }
+          *reinterpret_cast<uint4*>(dst + kc * KT_M * 16) = make_uint4(w[0], w[1], w[2], w[3]);
         }
-        *reinterpret_cast<uint4*>(dst + kc * KT_M * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+        fence_async_smem();
+        mbar_arrive(&full_a[s]);
+        load_u(k + PD, ub[d]);
       }
-      fence_async_smem();
-      mbar_arrive(&full_a[s]);
-#pragma unroll
-      for (int q = 0; q < UMAX; ++q) ucur[q] = unext[q];
     }
     // ---- epilogue: TMEM -> registers -> recombine planes -> atomics --------
     mbar_wait(done, 0);
