@@ -7,6 +7,7 @@ raises ``EngineUnavailable``.
 from __future__ import annotations
 
 import ctypes
+import functools
 import os
 import threading
 from collections import OrderedDict
@@ -139,10 +140,34 @@ def _c_rows(a, width=None):
     return a
 
 
+def _serialized(cls):
+    """Hold the owning engine's re-entrant lock for the whole of every public
+    method: a gw_ctx is single-submitter (include/gatewave_b200.h), but the
+    reference runtime calls eval_gate_batch from K pool threads at once
+    (runtime.py:184) and ctypes drops the GIL inside the call,
+    so concurrent callers of one cached engine are serialised here (the GPU
+    runs one batch at a time anyway) and each call's error text stays its own."""
+    for name, fn in list(vars(cls).items()):
+        if name.startswith("__") or name == "_check" or not callable(fn) or \
+                isinstance(fn, (staticmethod, classmethod, type)):
+            continue
+
+        def wrap(f):
+            @functools.wraps(f)
+            def locked(self, *a, **k):
+                with self._mtx:
+                    return f(self, *a, **k)
+            return locked
+        setattr(cls, name, wrap(fn))
+    return cls
+
+
+@_serialized
 class Engine:
     """One device context holding parameters and (optionally) keys."""
 
     def __init__(self, n, N, bg_bits, l, ks_base_bits, ks_levels, mu, device: int | None = None):
+        self._mtx = threading.RLock()
         self._lib = load_library()
         if device is None:
             device = default_device()
@@ -334,6 +359,7 @@ class Engine:
         return Plan(self, h, offs.shape[0] - 1)
 
 
+@_serialized
 class ExchangePlanHandle:
     """Device-resident exchange plan (gw_xplan): pack / unpack one level's wires."""
 
@@ -352,6 +378,10 @@ class ExchangePlanHandle:
                                                   self._ids.ctypes.data_as(_I64P), ctypes.byref(h)))
         self._h = h
 
+    @property
+    def _mtx(self):
+        return self.engine._mtx
+
     def pad(self, level: int) -> int:
         v = ctypes.c_int64(0)
         self.engine._check(self.engine._lib.gw_xplan_pad(self.engine._ctx, self._h, level, ctypes.byref(v)))
@@ -369,11 +399,16 @@ class ExchangePlanHandle:
             self._h = None
 
 
+@_serialized
 class Plan:
     def __init__(self, engine: Engine, handle, n_levels: int):
         self.engine = engine
         self._h = handle
         self.n_levels = n_levels
+
+    @property
+    def _mtx(self):
+        return self.engine._mtx
 
     def run(self, first: int = 0, last: int | None = None):
         last = self.n_levels if last is None else last

@@ -127,3 +127,30 @@ def test_exchange_pack_unpack_kernels(p128_keys):
     want[[20, 21]] = new
     assert np.array_equal(got, want)
     x.close()
+
+
+def test_concurrent_gate_batches_from_pool_threads(p128_keys):
+    """The reference runtime submits eval_gate_batch from K pool threads at once
+    (runtime.py:184); with the drop-in patched in, every thread shares one cached
+    engine.  Results must equal the sequential ones bit for bit."""
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_2306_11006_b200.cggi import GATE_ARITY, PARAM_128, GateKind, encrypt_bits, eval_gate_batch
+    from paper_2306_11006_b200.rng import SeededRng
+    ks = p128_keys
+    ek = ks.eval_key()
+    rng = np.random.default_rng(17)
+    kinds = [GateKind.NAND, GateKind.XOR, GateKind.AND, GateKind.MUX, GateKind.OR, GateKind.NOT,
+             GateKind.XNOR, GateKind.NOR]
+    jobs = []
+    for j, kind in enumerate(kinds):
+        ar = GATE_ARITY[kind]
+        B = 24 + 8 * j
+        ops = [encrypt_bits(PARAM_128, ks.lwe_sk, rng.integers(0, 2, B).astype(np.uint8), SeededRng(100 * j + k))
+               for k in range(ar)]
+        jobs.append((kind, ops))
+    want = [eval_gate_batch(kind, ops, ek) for kind, ops in jobs]
+    with ThreadPoolExecutor(max_workers=8) as pool:
+        for _ in range(2):
+            got = list(pool.map(lambda job: eval_gate_batch(job[0], job[1], ek), jobs))
+            for g, w in zip(got, want):
+                assert np.array_equal(g, w)

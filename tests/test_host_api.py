@@ -130,3 +130,15 @@ def test_gate_api_validates_before_touching_the_device(mini_keys):
         cggi.eval_gate_batch(GateKind.AND, [good, np.zeros((3, MINI.n + 1), np.uint32)], ek)
     with pytest.raises(DimensionError):
         cggi.eval_gate_batch(GateKind.CONST0, [], ek)
+
+
+def test_engine_methods_are_serialised():
+    """Every public method of the context wrappers holds the engine lock (a
+    gw_ctx is single-submitter; the reference runtime calls from K threads)."""
+    from paper_2306_11006_b200 import engine as E
+    for cls, names in ((E.Engine, ("eval_gate_batch", "blind_rotate", "keyswitch", "wires_put",
+                                   "wires_get", "plan_create", "sync", "upload_keys")),
+                       (E.Plan, ("run", "close")),
+                       (E.ExchangePlanHandle, ("pack", "unpack", "pad", "close"))):
+        for n in names:
+            assert hasattr(getattr(cls, n), "__wrapped__"), f"{cls.__name__}.{n} is not serialised"
