@@ -1,0 +1,95 @@
+"""pytest plugin: run the reference's OWN test-suite with its compiled kernels
+replaced by this engine.
+
+Seam 1 (default, GW_SEAM=1): `gatewave.cggi._blind_rotate_kernel` and
+`_keyswitch_kernel` (cggi.py:592-692) are module globals resolved at call time
+(callers cggi.py:715, 721, 744, 766, 837, 846), so every bootstrap the
+reference performs -- gates, MUX, single-sample wrappers, runtime.evaluate with
+K pool threads -- runs on the B200.  Seam 2 (GW_SEAM=2) additionally swaps
+`eval_gate_batch` itself (cggi.py:785, bound into runtime.py:26-33) for
+`paper_2306_11006_b200.cggi.eval_gate_batch`; its DimensionError / ParameterError
+(ValueError subclasses, like the reference's) are re-raised as the reference's
+classes, since a mixed process holds both packages' exception types.
+
+Every call is counted; a call the engine cannot take (unknown key array) falls
+back to the reference kernel and is reported, so the summary shows how much of
+the suite actually ran through the GPU.  Test infrastructure only.
+
+Usage (tools/ref_suite/run.sh): PYTHONPATH=baseline/_ref:tools/ref_suite:. \
+    python -m pytest baseline/_ref/_tests -p gw_seam
+"""
+import collections
+import os
+
+import numpy as np
+
+STATS = collections.Counter()
+_BK = {}
+
+
+def _params(n, N, bg_bits, l, ks_base_bits=2, ks_levels=8, mu=1 << 29):
+    class P:  # the attribute set engine.params_tuple reads
+        pass
+    p = P()
+    p.n, p.N, p.Bg_bits, p.l, p.ks_base_bits, p.ks_levels, p.mu = n, N, bg_bits, l, ks_base_bits, ks_levels, mu
+    return p
+
+
+def pytest_configure(config):
+    import gatewave.cggi as ref
+    from paper_2306_11006_b200 import engine
+
+    orig_init = ref.BootstrappingKey.__init__
+
+    def bk_init(self, *a, **k):
+        orig_init(self, *a, **k)
+        _BK[id(self.ntt)] = (self.ntt, self.data)  # keep ntt alive: ids stay unique
+
+    ref.BootstrappingKey.__init__ = bk_init
+    orig_br, orig_ks = ref._blind_rotate_kernel, ref._keyswitch_kernel
+
+    def blind_rotate_kernel(cts, tv, bk_ntt, psi_brv, ipsi_brv, n_inv, log_n, bg_bits, levels,
+                            dec_offset, counts):
+        hit = _BK.get(id(bk_ntt))
+        if hit is None or hit[0] is not bk_ntt:
+            STATS["blind_rotate_fallback"] += 1
+            return orig_br(cts, tv, bk_ntt, psi_brv, ipsi_brv, n_inv, log_n, bg_bits, levels,
+                           dec_offset, counts)
+        B, n, N = cts.shape[0], cts.shape[1] - 1, tv.shape[1]
+        eng = engine.engine_for(_params(n, N, bg_bits, levels), hit[1], None)
+        out = eng.blind_rotate(np.ascontiguousarray(cts, np.uint32), np.ascontiguousarray(tv, np.uint32))
+        counts[0] += 2 * levels * n * B  # the reference kernel's exact tallies (cggi.py:647, 660)
+        counts[1] += 2 * n * B
+        STATS["blind_rotate_gpu"] += 1
+        STATS["bootstraps_gpu"] += B
+        return out
+
+    def keyswitch_kernel(exts, ksk, levels, gamma):
+        N, n = ksk.shape[0], ksk.shape[3] - 1
+        eng = engine.engine_for(_params(n, N, 9, 2, gamma, levels), None, ksk)
+        STATS["keyswitch_gpu"] += 1
+        return eng.keyswitch(np.ascontiguousarray(exts, np.uint32))
+
+    ref._blind_rotate_kernel = blind_rotate_kernel
+    ref._keyswitch_kernel = keyswitch_kernel
+    if os.environ.get("GW_SEAM", "1") == "2":
+        import gatewave.runtime as rt
+        from paper_2306_11006_b200 import cggi as mine
+
+        def eval_gate_batch(kind, operands, ek, counter=None, count=None):
+            STATS["eval_gate_batch_gpu"] += 1
+            try:
+                return mine.eval_gate_batch(kind, operands, ek, counter=counter, count=count)
+            except mine.DimensionError as e:  # same meaning, the caller's class (cggi.py:51)
+                raise ref.DimensionError(str(e)) from e
+            except mine.ParameterError as e:
+                raise ref.ParameterError(str(e)) from e
+
+        ref.eval_gate_batch = eval_gate_batch
+        rt.eval_gate_batch = eval_gate_batch
+
+
+def pytest_terminal_summary(terminalreporter, exitstatus, config):
+    terminalreporter.section("gatewave-b200 seam")
+    terminalreporter.write_line(f"GW_SEAM={os.environ.get('GW_SEAM', '1')}: " +
+                                ", ".join(f"{k}={v}" for k, v in sorted(STATS.items())))
