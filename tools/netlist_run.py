@@ -48,7 +48,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, required=True)
     ap.add_argument("--repeats", type=int, default=2)
+    ap.add_argument("--vectors", type=int, default=None,
+                    help="input vectors per netlist, each evaluated on its own (default: 100 for "
+                         "config 2 -- the tests/test_acceptance.py:349-362 pattern -- else 1)")
     args = ap.parse_args()
+    if args.vectors is None:
+        args.vectors = 100 if args.config == 2 else 1
 
     import torch
     ws = int(os.environ.get("WORLD_SIZE", "1"))
@@ -109,13 +114,34 @@ def main():
         ok = all(np.array_equal(decrypt_rows(ks.lwe_sk, outs[k]), plain[k][:, 0]) for k in plain)
         prep["plain_check_s"] = time.monotonic() - t
         nb = bootstraps_of(sched)
+        per_vec = None
+        if args.vectors > 1:
+            # vectors 1..V-1: fresh plaintexts from the same generator, SeededRng(8000 + v)
+            vl, vok = [app], [bool(ok)]
+            for v in range(1, args.vectors):
+                vb = {p.name: rng.integers(0, 2, p.width).astype(np.uint8) for p in c.inputs}
+                vr = SeededRng(8000 + v)
+                vin = {p.name: encrypt_bits(P, ks.lwe_sk, vb[p.name], vr) for p in c.inputs}
+                if ws > 1:
+                    torch.distributed.barrier()
+                torch.cuda.synchronize()
+                t = time.monotonic()
+                vo, _ = evaluate(c, sched, vin, ek)
+                torch.cuda.synchronize()
+                vl.append(time.monotonic() - t)
+                vp = C.simulate_plain_bits(c, {k: x[:, None] for k, x in vb.items()})
+                vok.append(all(np.array_equal(decrypt_rows(ks.lwe_sk, vo[k]), vp[k][:, 0]) for k in vp))
+            a = np.asarray(vl)
+            per_vec = {"vectors": args.vectors, "decrypt_ok": int(sum(vok)),
+                       "latency_mean_s": float(a.mean()), "latency_p50_s": float(np.median(a)),
+                       "latency_p90_s": float(np.quantile(a, 0.9)), "latency_max_s": float(a.max())}
         results.append({
             "netlist": name, "gates": len(c.gates), "bootstraps": nb, "levels": len(sched.waves),
             "max_level_gates": max(sum(len(b.gate_ids) for b in w) for w in sched.waves),
             "app_latency_s": app, "app_latency_first_s": lat[0], "gates_per_s": len(c.gates) / app, "bootstraps_per_s": nb / app,
             "device_time_s": met.device_time_seconds, "decrypt_ok": bool(ok),
             "input_bits": int(sum(p.width for p in c.inputs)), "output_bits": int(sum(p.width for p in c.outputs)),
-            "host_prep": prep})
+            "host_prep": prep, **({"per_vector": per_vec} if per_vec else {})})
     if rank == 0:
         print(json.dumps({"config": args.config, "n_gpus": ws, "params": "PARAM_128",
                           "keygen_and_upload_s": t_keys, "results": results}), flush=True)
