@@ -286,18 +286,6 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
   const int mc0 = 4 * o + 2 * (lane >> 4);
   const int pos = v3_pos(l);
   const int bar_id = 1 + gl;
-  // lane twiddles for one transform, from TMEM into registers
-  auto load_tw = [&](double2 (&tw)[P]) {
-    uint32_t r[2][32];
-    tm_ld_raw<32>(tm_tw, r[0]);
-    tm_ld_raw<32>(tm_tw + 32, r[1]);
-    tm_wait_ld();
-#pragma unroll
-    for (int k1 = 0; k1 < P; ++k1) {
-      const uint32_t* w = r[k1 >> 3] + (k1 & 7) * 4;
-      tw[k1] = make_double2(__hiloint2double(w[1], w[0]), __hiloint2double(w[3], w[2]));
-    }
-  };
   int sc = 0;  // ring slot base of step i: (4 i) mod 7
 
   const bool prof = a.prof != nullptr && blockIdx.x == 0 && gl == 0 && lane == 0;
@@ -413,11 +401,9 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
       }
       if (GC == 2 && kStagger && i == 0 && gl == 0 && lane == 0) mbar_arrive(&go_bar[0]);
       double2* tile = U + (size_t)o * P * L;
-      if constexpr (GC <= 2) {
-        double2 tw[P];
-        load_tw(tw);
-        fft_forward_head<LOGN, true>(x, tile, TwRegs<P>{tw}, l);
-      } else if constexpr (!kTwSmem) {
+      // lane twiddles streamed from TMEM in chunks during the twiddle multiply
+      // (measured: GC = 1 -1.5 % per step against loading all 16 up front; GC = 2 neutral)
+      if constexpr (!kTwSmem) {
         fft_forward_head<LOGN, true>(x, tile, TwTmemHalves{tm_tw}, l);
       } else {
         fft_forward_head<LOGN, true>(x, tile, TwSmem{tw1, L, l}, l);
@@ -495,11 +481,7 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
       double2* tile = U + (size_t)o * P * L;
 #pragma unroll
       for (int c = 0; c < P; ++c) x[bitrev_c<G::LOGP>(c)] = tile[c * L + pos];
-      if constexpr (GC <= 2) {
-        double2 tw[P];
-        load_tw(tw);
-        fft_inverse_tail<LOGN, true>(x, tile, TwRegs<P>{tw}, l);
-      } else if constexpr (!kTwSmem) {
+      if constexpr (!kTwSmem) {
         fft_inverse_tail<LOGN, true>(x, tile, TwTmemHalves{tm_tw}, l);
       } else {
         fft_inverse_tail<LOGN, true>(x, tile, TwSmem{tw1, L, l}, l);
