@@ -21,6 +21,7 @@ phase2) for g in 256 592; do GATEWAVE_BR_KERNEL=v2 timeout 300 python tools/phas
 brtime) timeout 300 python tools/br_time.py > gpurun_out/${TAG}_brtime.txt 2>&1 ;;
 gcq) for gc in 1 2 4; do echo "GC=$gc"; GATEWAVE_BR_GC=$gc timeout 300 python tools/br_time.py 148 256 592 2368; done > gpurun_out/${TAG}_gcq.txt 2>&1 ;;
 ab) for v in $(ls variants/*.so); do for gc in ${ABGC:-2 4}; do echo "$v GC=$gc"; GATEWAVE_B200_LIB=$v GATEWAVE_BR_GC=$gc timeout 300 python tools/br_time.py 256 2368; done; done > gpurun_out/${TAG}_ab.txt 2>&1 ;;
+refsuite) for seam in 1 2; do timeout 1500 tools/ref_suite/run.sh run $seam > gpurun_out/${TAG}_refsuite$seam.txt 2>&1; done ;;  # stage first: tools/ref_suite/run.sh stage
 gcsweep) for gc in 1 2 3 4; do echo "GC=$gc"; GATEWAVE_BR_GC=$gc timeout 300 python tools/br_time.py 148 256 444 592 1184 2368; done > gpurun_out/${TAG}_gcsweep.txt 2>&1 ;;
 esac
 done
