@@ -154,3 +154,19 @@ def test_concurrent_gate_batches_from_pool_threads(p128_keys):
             got = list(pool.map(lambda job: eval_gate_batch(job[0], job[1], ek), jobs))
             for g, w in zip(got, want):
                 assert np.array_equal(g, w)
+
+
+def test_eval_key_file_feeds_the_device(p128_keys, tmp_path):
+    """An ARFX evaluation key (reference format) loads straight onto the GPU and
+    gives the same gate outputs as the in-memory keys."""
+    from paper_2306_11006_b200 import serial as S
+    from paper_2306_11006_b200.cggi import PARAM_128, GateKind, encrypt_bits, eval_gate_batch
+    from paper_2306_11006_b200.rng import SeededRng
+    path = str(tmp_path / "p128.ek")
+    S.write_eval_key(path, p128_keys)
+    ek = S.read_eval_key(path, upload=True)
+    rng = np.random.default_rng(5)
+    a = encrypt_bits(PARAM_128, p128_keys.lwe_sk, rng.integers(0, 2, 40).astype(np.uint8), SeededRng(1))
+    b = encrypt_bits(PARAM_128, p128_keys.lwe_sk, rng.integers(0, 2, 40).astype(np.uint8), SeededRng(2))
+    assert np.array_equal(eval_gate_batch(GateKind.XOR, [a, b], ek),
+                          eval_gate_batch(GateKind.XOR, [a, b], p128_keys.eval_key()))
