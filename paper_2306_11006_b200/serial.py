@@ -31,7 +31,7 @@ from typing import BinaryIO, Mapping
 
 import numpy as np
 
-from .cggi import EvalKey, KeySet, ParamSet, SecretKey
+from .cggi import EvalKey, KeySet, ParamSet, SecretKey  # noqa: F401  (KeySet: annotations)
 
 MAGIC = b"ARFX"
 FORMAT_VERSION = 1
@@ -134,7 +134,7 @@ def _write(path: str, chunks) -> None:
 # -- secret keys --------------------------------------------------------------
 
 def write_secret_key(path: str, key: SecretKey | KeySet) -> None:
-    sk = key.secret_key() if isinstance(key, KeySet) else key
+    sk = key.secret_key() if hasattr(key, "secret_key") else key  # KeySet (ours or the reference's)
     _write(path, (_header_bytes(KIND_SECRET), params_to_bytes(sk.params),
                   _le(sk.lwe_sk, "u1"), _le(sk.rlwe_sk, "u1")))
 
@@ -157,7 +157,7 @@ def _key_shapes(p: ParamSet):
 
 
 def write_eval_key(path: str, keys: KeySet | EvalKey) -> None:
-    ek = keys.eval_key() if isinstance(keys, KeySet) else keys
+    ek = keys.eval_key() if hasattr(keys, "eval_key") else keys
     _write(path, (_header_bytes(KIND_EVAL), params_to_bytes(ek.params),
                   _le(ek.bk.data, "<u4"), _le(ek.ksk.data, "<u4")))
 
