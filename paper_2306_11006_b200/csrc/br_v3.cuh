@@ -28,6 +28,10 @@
 #include "mbarrier.cuh"
 #include "tmem.cuh"
 
+#ifndef GW_STAGGER2
+#define GW_STAGGER2 1  // GC = 2: gate 1 starts after gate 0's decomposition (0), F (1) or M (2) of step 0
+                        // (same-box A/B: 9.54k / 9.39k / 9.64k cycles per step)
+#endif
 #ifndef GW_TW_SMEM_GC
 #define GW_TW_SMEM_GC 5  // smallest GC that keeps the lane twiddles in shared memory (none: TMEM measured faster at GC=4 too)
 #endif
@@ -339,10 +343,10 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
     }
   } else {
   if constexpr (LDR && GC >= 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(CREG));
-  // Stagger (measured: GC = 3 +1 %, GC = 2 +0-7 %): the gates of a CTA start at
+  // Stagger (measured: GC = 3 +1 %, GC = 2 +1.6-8 %): the gates of a CTA start at
   // different points of step 0 so they run different phases at once.  GC = 3:
   // gate 1 after gate 0's F(0), gate 2 after its M(0); GC = 2: gate 1 after gate
-  // 0's digit decomposition (its integer work then overlaps gate 0's FFTs).
+  // 0's F(0) (GW_STAGGER2).
   constexpr bool kStagger = LDR && (GC == 3 || GC == 2);
   if (kStagger && gl >= 1) mbar_wait(&go_bar[gl - 1], 0);
   uint32_t a_next = __ldg(lin_g);
@@ -399,7 +403,7 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
           x[bitrev_c<G::LOGP>(m1 + q)] = v;  // DIT forward takes bit-reversed input
         }
       }
-      if (GC == 2 && kStagger && i == 0 && gl == 0 && lane == 0) mbar_arrive(&go_bar[0]);
+      if (GC == 2 && GW_STAGGER2 == 0 && kStagger && i == 0 && gl == 0 && lane == 0) mbar_arrive(&go_bar[0]);
       double2* tile = U + (size_t)o * P * L;
       // lane twiddles streamed from TMEM in chunks during the twiddle multiply
       // (measured: GC = 1 -1.5 % per step against loading all 16 up front; GC = 2 neutral)
@@ -412,7 +416,8 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
 #pragma unroll
       for (int c = 0; c < P; ++c) tile[c * L + pos] = x[c];
     }
-    if (GC == 3 && kStagger && i == 0 && gl == 0 && lane == 0) mbar_arrive(&go_bar[0]);
+    if ((GC == 3 || (GC == 2 && GW_STAGGER2 == 1)) && kStagger && i == 0 && gl == 0 && lane == 0)
+      mbar_arrive(&go_bar[0]);
     mark(0);
     if (KM == 0 && pre) {  // buffer nxt is free once every warp finished MAC(i-1)
       if (i >= 1) mbar_wait(&empty_bar[nxt], (uint32_t)(((i - 1) >> 1) & 1));
@@ -468,6 +473,7 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
     }
     release(&empty_bar[cur]);
     if (kStagger && i == 0 && gl == 0 && lane == 0) mbar_arrive(&go_bar[1]);
+    if (GC == 2 && GW_STAGGER2 == 2 && kStagger && i == 0 && gl == 0 && lane == 0) mbar_arrive(&go_bar[0]);
     mark(2);
     if (pre) {
       kstore(i, sn, 1);
