@@ -32,6 +32,21 @@
 #define GW_STAGGER2 1  // GC = 2: gate 1 starts after gate 0's decomposition (0), F (1) or M (2) of step 0
                         // (same-box A/B: 9.54k / 9.39k / 9.64k cycles per step)
 #endif
+// Loader-warp register budget and loads in flight per round at 2 / 3 gates per CTA.
+// Same-box A/B (cycles per step): GC=2 LREG 64 + RS 16 9.40k, LREG 56 9.64k, LREG 104 +
+// RS 24 9.76k; GC=3 LREG 56 12.64k, 64 12.94k, 40 13.17k, RS 8 14.7k, RS 12 17.7k.
+#ifndef GW_LREG2
+#define GW_LREG2 64
+#endif
+#ifndef GW_LREG3
+#define GW_LREG3 56
+#endif
+#ifndef GW_RS2
+#define GW_RS2 16
+#endif
+#ifndef GW_RS3
+#define GW_RS3 16
+#endif
 #ifndef GW_TW_SMEM_GC
 #define GW_TW_SMEM_GC 5  // smallest GC that keeps the lane twiddles in shared memory (none: TMEM measured faster at GC=4 too)
 #endif
@@ -119,8 +134,10 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
   static_assert(!LDR || GC <= 3, "loader warps need registers the compute warps can spare");
   // with loader warps at GC >= 2 the register file is re-split with setmaxnreg:
   // compute warpgroups CREG, the loader warpgroup LREG (CREG*128*GC + LREG*128 <= 64K)
-  constexpr int LREG = GC == 1 ? 0 : GC == 2 ? 64 : 56;
-  constexpr int CREG = GC == 1 ? 0 : GC == 2 ? 216 : 152;
+  constexpr int LREG = GC == 1 ? 0 : GC == 2 ? GW_LREG2 : GW_LREG3;
+  // the register pool is what the launch allocated: (64K / threads) rounded down to 8, per thread
+  constexpr int kPool = ((65536 / (128 * GC + 128)) & ~7) * (128 * GC + 128);
+  constexpr int CREG = GC == 1 ? 0 : ((kPool - LREG * 128) / (128 * GC)) & ~7;
   using G = V3::G;
   constexpr int N = V3::N, M = V3::M, P = V3::P, L = V3::L, R = V3::R, LEV = V3::LEV, LOGN = V3::LOGN;
   constexpr int UB = V3::UB, COLS = V3::COLS, CIDX = V3::CIDX;
@@ -306,7 +323,7 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
   if (LDR && warp >= 4 * GC) {
     // ---- loader warp: slab i -> ring slots of sub-partition o, ahead of the MAC ----
     if constexpr (LDR && GC >= 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(LREG));
-    constexpr int RS = GC == 1 ? 24 : 16;  // loads in flight per round
+    constexpr int RS = GC == 1 ? 24 : GC == 2 ? GW_RS2 : GW_RS3;  // loads in flight per round (divides 48)
     const double2* src_w = a.bk + (size_t)32 * o + lane;
     int s_i = 0;
     for (int i = 0; i < a.n; ++i) {
