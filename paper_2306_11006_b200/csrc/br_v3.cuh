@@ -47,6 +47,14 @@
 #ifndef GW_RS3
 #define GW_RS3 16
 #endif
+// Loader warps: one thread per CTA prefetches the key slab GW_L2PF steps ahead into L2
+// (cp.async.bulk.prefetch).  Same-box A/B, cycles per step: GC=2 9.41k -> 9.23k at distance
+// 2, 4 or 6 (1 and 3 are 9-10 % slower); GC=1 -0.3 %, GC=3 neutral.  With the transform work
+// ablated, GC=2 drops from 8.86k to 7.43k: the L2 latency of the key loads is what bounds the
+// step once the compute gets faster.
+#ifndef GW_L2PF
+#define GW_L2PF 2
+#endif
 #ifndef GW_TW_SMEM_GC
 #define GW_TW_SMEM_GC 5  // smallest GC that keeps the lane twiddles in shared memory (none: TMEM measured faster at GC=4 too)
 #endif
@@ -328,6 +336,13 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
     int s_i = 0;
     for (int i = 0; i < a.n; ++i) {
       const double2* src = src_w + (size_t)i * CIDX * 128;
+#if GW_L2PF
+      // one thread per CTA asks L2 for slab i + GW_L2PF ahead of every SM's loads
+      if (o == 0 && lane == 0 && i + GW_L2PF < a.n) {
+        const char* pf = reinterpret_cast<const char*>(a.bk + (size_t)(i + GW_L2PF) * CIDX * 128);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf), "r"(V3::SLAB) : "memory");
+      }
+#endif
       if (i >= 2) {  // chunks 0-2 reuse the slots of slab i-2's chunks 1-3
         mbar_wait(&empty_bar[i & 1], (uint32_t)(((i - 2) >> 1) & 1));
         tm_fence_after();
@@ -367,6 +382,7 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
   constexpr bool kStagger = LDR && (GC == 3 || GC == 2);
   if (kStagger && gl >= 1) mbar_wait(&go_bar[gl - 1], 0);
   uint32_t a_next = __ldg(lin_g);
+  uint32_t sink = 0;  // GW_ABL & 8 only
   for (int i = 0; i < a.n; ++i) {
     const int cur = i & 1, nxt = cur ^ 1;
     const int sn = kRing ? (sc + 4 >= V3::RING ? sc + 4 - V3::RING : sc + 4) : 4 - sc;  // slot base of step i+1
@@ -393,6 +409,13 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
       const uint32_t* from_partner = xg + (size_t)lv * (P / 2) * 32;
       uint32_t mine[P];
       const uint32_t idxh = idx0 + (uint32_t)(hh * M);
+#if GW_ABL & 1
+#pragma unroll
+      for (int m1 = 0; m1 < P; ++m1) mine[m1] = (idxh + (uint32_t)(7 * m1)) & base_mask;
+#pragma unroll
+      for (int m1 = 0; m1 < P; m1 += 2) {
+        const uint32_t w = (mine[m1] * 3u) | (mine[m1 + 1] << 16);
+#else
 #pragma unroll
       for (int m1 = 0; m1 < P; m1 += 2) {
         uint32_t oth[2];
@@ -411,6 +434,7 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
 #pragma unroll
       for (int m1 = 0; m1 < P; m1 += 2) {
         const uint32_t w = from_partner[(m1 / 2) * 32 + lane];
+#endif
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const uint32_t rv = q ? (w >> 16) : (w & 0xFFFFu);
@@ -467,6 +491,10 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
       double2 O[4][2];  // [output][s]
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
+#if GW_ABL & 4
+#pragma unroll
+        for (int oo = 0; oo < 4; ++oo) O[oo][s] = D[oo][s];
+#else
         uint32_t kw[2][32];
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf)
@@ -480,6 +508,7 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
             const double2 kr = make_double2(__hiloint2double(k4[1], k4[0]), __hiloint2double(k4[3], k4[2]));
             O[oo][s] = r == 0 ? cmul(D[r][s], kr) : cfma(O[oo][s], D[r][s], kr);
           }
+#endif
       }
 #pragma unroll
       for (int oo = 0; oo < 4; ++oo) {
@@ -520,8 +549,13 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
         for (int m1 = 0; m1 < P; ++m1) {
           const double2 v = m1 == 0 ? x[0] : cmulc(x[m1], c_root64[G::CSTEP * m1]);
           const uint32_t j = (uint32_t)(L * m1 + l);
+#if GW_ABL & 8
+          sink ^= (round_mod32(v.x) << shift) + round_mod32(v.y);
+          (void)j;
+#else
           atomicAdd(Ac + j, round_mod32(v.x) << shift);
           atomicAdd(Ac + j + M, round_mod32(v.y) << shift);
+#endif
         }
       }
     }
@@ -545,6 +579,10 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
     mark(5);
     sc = sn;
   }
+#if GW_ABL & 8
+  if (active) atomicXor(acc_g, sink);
+#endif
+  (void)sink;
   if (prof)
     for (int ph = 0; ph < 6; ++ph) a.prof[o * 6 + ph] = pt_[ph];
   if (active && o < 2) {

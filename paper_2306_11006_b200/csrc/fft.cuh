@@ -17,6 +17,9 @@
 // these index maps in numpy.
 #pragma once
 #include "gw_common.cuh"
+#ifndef GW_ABL
+#define GW_ABL 0  // timing-only ablations (tools): 1 decomposition, 2 transposes, 4 MAC, 8 atomics
+#endif
 
 namespace gw {
 
@@ -256,6 +259,7 @@ __device__ __forceinline__ void fft_forward_head(double2 (&x)[Geo<LOGN>::P], dou
   dit<P, +1>(x);
 #pragma unroll
   for (int k1 = TW0 ? 0 : 1; k1 < P; ++k1) x[k1] = cmul(x[k1], tw(k1));
+#if !(GW_ABL & 2)
   __syncwarp();
 #pragma unroll
   for (int k1 = 0; k1 < P; ++k1) tile[k1 * L + swz(k1, l)] = x[k1];
@@ -266,6 +270,7 @@ __device__ __forceinline__ void fft_forward_head(double2 (&x)[Geo<LOGN>::P], dou
     for (int a = 0; a < P; ++a) x[bitrev_c<LOGP>(a)] = tile[k1 * L + swz(k1, b + 2 * a)];
   }
   __syncwarp();
+#endif
   dit<P, +1>(x);  // x[c] = u_b[c]
 }
 
@@ -275,6 +280,7 @@ __device__ __forceinline__ void fft_inverse_tail(double2 (&x)[Geo<LOGN>::P], dou
   using G = Geo<LOGN>;
   constexpr int P = G::P, L = G::L, LOGP = G::LOGP;
   dit<P, -1>(x);  // x[a]
+#if !(GW_ABL & 2)
   __syncwarp();
   {
     const int k1 = l >> 1, b = l & 1;
@@ -285,6 +291,7 @@ __device__ __forceinline__ void fft_inverse_tail(double2 (&x)[Geo<LOGN>::P], dou
 #pragma unroll
   for (int k1 = 0; k1 < P; ++k1) x[bitrev_c<LOGP>(k1)] = tile[k1 * L + swz(k1, l)];
   __syncwarp();
+#endif
 #pragma unroll
   for (int k1 = TW0 ? 0 : 1; k1 < P; ++k1) {
     const int r = bitrev_c<LOGP>(k1);

@@ -286,7 +286,7 @@ int launch_v3_g(gw_ctx* c, const BrArgs& a0) {
 // GC=1 7.8k (loader warps), GC=2 9.6k, GC=3 12.6k (loader warps + setmaxnreg + stagger),
 // GC=4 17.7k (LDG key streaming by the compute warps).
 int launch_v3(gw_ctx* c, const BrArgs& a) {
-  static const double kStep[5] = {0, 7.8, 9.4, 12.6, 17.7};
+  static const double kStep[5] = {0, 7.8, 9.2, 12.6, 17.7};
   int gc = 1;
   double best = 1e300;
   for (int g = 1; g <= 4; ++g) {
