@@ -51,7 +51,8 @@
 // (cp.async.bulk.prefetch).  Same-box A/B, cycles per step: GC=2 9.41k -> 9.23k at distance
 // 2, 4 or 6 (1 and 3 are 9-10 % slower); GC=1 -0.3 %, GC=3 neutral.  With the transform work
 // ablated, GC=2 drops from 8.86k to 7.43k: the L2 latency of the key loads is what bounds the
-// step once the compute gets faster.
+// step once the compute gets faster.  Splitting the prefetch so each CTA requests only its
+// 1/148 share of the slab is slower (GC=2 9.43k): every CTA prefetching the whole slab wins.
 #ifndef GW_L2PF
 #define GW_L2PF 2
 #endif
