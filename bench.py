@@ -20,8 +20,21 @@ inputs of SURVEY.md Appendix A.  With N GPUs every rank evaluates its own
 * roofline   -- the blind-rotation kernel against the FP64 pipe: algorithmic
                 FLOPs (249,856 n per bootstrap) / its live
                 event-timed duration, vs the DFMA peak measured on this pool.
-* cpu_baseline / --impl reference -- the C restatement of the reference's
-                algorithm (oracle/, "port") on the host cores.
+* cpu_baseline / --impl reference -- the UNMODIFIED reference (numba,
+                pip-installed into baseline/_ref) through its own
+                runtime.evaluate on all host cores ("reference"); the C
+                restatement (oracle/, rebuilt -march=native for the host,
+                "port") only when baseline/_ref cannot be imported.  Config-2
+                CPU app latency is measured the same way; configs 3-5 are
+                extrapolated from the measured per-bootstrap cost and the
+                netlists' per-level bootstrap counts (labelled).
+* --gpus N   -- one process per GPU: under torchrun (WORLD_SIZE must equal N)
+                or, without it, bench.py re-launches itself under
+                torch.distributed.run.  Besides the per-rank config-1 batches
+                (weak scaling), N > 1 evaluates config 4 (and config 5 at N = 8)
+                sharded by netlist level across the N GPUs with the NCCL
+                point-to-point wire exchange, and reports its app latency,
+                exchange bytes and an output digest that must not depend on N.
 """
 from __future__ import annotations
 
@@ -54,7 +67,21 @@ def _args():
     ap.add_argument("--gates", type=int, default=GATES)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-netlist", action="store_true")
+    ap.add_argument("--sharded", default="auto",
+                    help="netlists evaluated sharded over the GPUs: auto (config4 at N>1, + config5 at "
+                         "N=8), none, or a comma list of config4,config5,config3")
+    ap.add_argument("--no-cpu-netlists", action="store_true")
     return ap.parse_args()
+
+
+def config_dict(gates: int, n_gpus: int) -> dict:
+    """The workload description both arms print (identical, so the driver can
+    match them)."""
+    return {"workload": f"config1: {gates} independent NAND gate bootstraps per GPU, "
+                        "PARAM_128 (n=630, N=1024, l=2, Bg=2^9, t=8, gamma=2)",
+            "gates_per_gpu": gates, "bootstraps_per_gate": 1,
+            "l2": "flushed (512 MB write) between timed GPU steps",
+            "parallelism": f"dp{n_gpus} (independent gate batches per GPU)"}
 
 
 def _dist():
@@ -137,16 +164,6 @@ class ClockSampler:
                 "reasons": sorted(self.reasons)}
 
 
-def cpu_oracle_run(params, ks, A, B, threads: int):
-    """Time the oracle (C restatement of the reference path) on host cores."""
-    import oracle as O
-    keys = O.Keys.from_params(params, ks.bootstrapping_key.data, ks.keyswitch_key.data)
-    t0 = time.perf_counter()
-    out = O.eval_gate_batch("NAND", [A, B], keys, threads=threads)
-    dt = time.perf_counter() - t0
-    return out, dt
-
-
 def _load_reference():
     """The unmodified reference package, pip-installed into baseline/_ref
     (DESIGN.md §6); None if it is not there."""
@@ -154,7 +171,8 @@ def _load_reference():
     if not os.path.isdir(os.path.join(path, "gatewave")):
         return None
     os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/gatewave_numba_cache")
-    sys.path.insert(0, path)
+    if path not in sys.path:
+        sys.path.insert(0, path)
     try:
         import gatewave.cggi  # noqa: F401
         import gatewave.circuit  # noqa: F401
@@ -165,6 +183,105 @@ def _load_reference():
         return None
 
 
+class CpuReference:
+    """The reference's own CPU path on this host: `runtime.evaluate(c,
+    build_schedule(c, K), inputs, keys)` with K = os.cpu_count() workers
+    (BASELINE.md CPU-baseline plan).  Falls back to the oracle port (rebuilt
+    -march=native here) when baseline/_ref cannot be imported."""
+
+    def __init__(self, gates: int):
+        from paper_2306_11006_b200.cggi import PARAM_128
+        self.model, self.cores = _cpu_info()
+        self.G = gates
+        self.ks, self.A, self.B, _, _ = _workload(PARAM_128, 0, gates)
+        self.ref = _load_reference()
+        self.kind = "reference" if self.ref is not None else "port"
+        if self.ref is not None:
+            from gatewave import cggi as rc, circuit as rcirc, scheduler as rsch
+            self.rc, self.rcirc, self.rsch = rc, rcirc, rsch
+            from gatewave import runtime as rrt
+            self.rrt = rrt
+            self.rks = rc.keygen(rc.PARAM_128, seed=7)      # same bytes as ours (tests pin the digests)
+            self.c1 = rcirc.gen_flat(gates, rc.GateKind.NAND)
+            self.s1 = rsch.build_schedule(self.c1, self.cores)
+        else:
+            import oracle as O
+            import oracle.oracle as OO
+            OO.use_native()
+            self.okeys = O.Keys.from_params(PARAM_128, self.ks.bootstrapping_key.data,
+                                            self.ks.keyswitch_key.data)
+
+    def step(self):
+        """One full config-1 batch; returns (outputs, seconds)."""
+        t0 = time.perf_counter()
+        if self.ref is not None:
+            outs, _ = self.rrt.evaluate(self.c1, self.s1, {"a": self.A, "b": self.B}, self.rks)
+            out = outs["y"]
+        else:
+            import oracle as O
+            out = O.eval_gate_batch("NAND", [self.A, self.B], self.okeys, threads=self.cores)
+        return out, time.perf_counter() - t0
+
+    def sample(self) -> str:
+        if self.ref is not None:
+            return (f"full config-1 batch ({self.G} NAND) per step through the unmodified reference "
+                    f"(baseline/_ref gatewave.runtime.evaluate, K={self.cores} workers, numba JIT warm) "
+                    f"on {self.model}")
+        return (f"full config-1 batch ({self.G} NAND) per step; oracle/gw_oracle.c -march=native on "
+                f"{self.cores} threads of {self.model} (baseline/_ref unavailable)")
+
+    def config2(self, repeats: int = 3):
+        """Config 2 app latency on the CPU: adder8 + 8x8 multiplier, median of
+        `repeats` full runs each (reference runtime, K = cores)."""
+        if self.ref is None:
+            return None
+        from paper_2306_11006_b200 import circuit as C
+        from paper_2306_11006_b200 import netlists as NL
+        from paper_2306_11006_b200.cggi import PARAM_128, encrypt_bits
+        from paper_2306_11006_b200.rng import SeededRng
+        res = {}
+        rng = np.random.default_rng(80)
+        for name, c in (("adder8", C.gen_adder(8)), ("multiplier8", NL.gen_multiplier(8))):
+            vals = {p.name: int(rng.integers(0, 1 << p.width)) for p in c.inputs}
+            srng = SeededRng(8000)
+            inputs = {p.name: encrypt_bits(PARAM_128, self.ks.lwe_sk, C.value_to_bits(vals[p.name], p.width),
+                                           srng) for p in c.inputs}
+            rcirc = self.rcirc.parse_circuit(C.serialize_circuit(c))
+            sched = self.rsch.build_schedule(rcirc, self.cores)
+            lat = []
+            for _ in range(repeats):
+                t0 = time.perf_counter()
+                self.rrt.evaluate(rcirc, sched, inputs, self.rks)
+                lat.append(time.perf_counter() - t0)
+            res[name] = {"app_latency_s": statistics.median(lat), "gates": len(c.gates), "repeats": repeats}
+        res["total_app_latency_s"] = sum(v["app_latency_s"] for v in res.values())
+        res["workers"] = self.cores
+        return res
+
+    def extrapolated_netlists(self, per_bootstrap_s: float):
+        """Configs 3-5 on the CPU, EXTRAPOLATED: level L costs ceil(b_L / K)
+        serial bootstraps of one worker, at the per-bootstrap time measured on
+        this host (config-1 batch through the reference runtime)."""
+        try:
+            with open(os.path.join(ROOT, "tools", "level_profiles.json")) as f:
+                prof = json.load(f)
+        except OSError:
+            return None
+        out = {}
+        K = self.cores
+        for name, p in prof.items():
+            if not name.startswith(("config3", "config4", "config5")):
+                continue
+            t = sum(-(-b // K) * per_bootstrap_s for b in p["bootstraps_per_level"])
+            boots = sum(p["bootstraps_per_level"])
+            out[name] = {"app_latency_s": t, "gates_per_s": p["gates"] / t, "bootstraps_per_s": boots / t,
+                         "gates": p["gates"], "levels": p["levels"], "extrapolated": True}
+        out["method"] = (f"extrapolated: sum over levels of ceil(bootstraps_L / K) x {per_bootstrap_s * 1e3:.1f} ms "
+                         f"(one worker's per-bootstrap time, measured here on the config-1 batch), K = {K}; "
+                         "level profiles from tools/level_profiles.json")
+        return out
+
+
 def run_reference(args):
     """Reference arm: the reference's own CPU implementation of the path on all
     host cores -- `runtime.evaluate(gen_flat(256, NAND), build_schedule(c, K))`
@@ -173,46 +290,21 @@ def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
         return 0
-    from paper_2306_11006_b200.cggi import PARAM_128
-    model, cores = _cpu_info()
-    ks, A, B, _, _ = _workload(PARAM_128, 0, args.gates)
-    ref = _load_reference()
-    if ref is not None:
-        from gatewave import cggi as rc, circuit as rcirc, runtime as rrt, scheduler as rsch
-        rks = rc.keygen(rc.PARAM_128, seed=7)       # same bytes as ours (tests pin the digests)
-        c = rcirc.gen_flat(args.gates, rc.GateKind.NAND)
-        sched = rsch.build_schedule(c, cores)
-        inputs = {"a": A, "b": B}
-
-        def step():
-            t0 = time.perf_counter()
-            outs, _ = rrt.evaluate(c, sched, inputs, rks)
-            return outs["y"], time.perf_counter() - t0
-        kind = "reference"
-        sample = (f"full config-1 batch ({args.gates} NAND) per step through the unmodified "
-                  f"reference (baseline/_ref gatewave.runtime.evaluate, K={cores} workers, "
-                  f"numba JIT warm) on {model}")
-    else:
-        def step():
-            return cpu_oracle_run(PARAM_128, ks, A, B, cores)
-        kind = "port"
-        sample = (f"full config-1 batch ({args.gates} NAND) per step; oracle/gw_oracle.c on "
-                  f"{cores} threads of {model} (baseline/_ref unavailable)")
+    cpu = CpuReference(args.gates)
     for _ in range(max(args.warmup, 1)):
-        step()
-    times = [step()[1] for _ in range(args.steps)]
+        cpu.step()
+    times = [cpu.step()[1] for _ in range(args.steps)]
     mean = statistics.mean(times)
     value = args.gates / mean
     line = {
         "impl": "reference", "metric": "bootstrapped gates/sec", "value": value, "unit": "gates/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": mean * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u64 (Goldilocks NTT)", "data": "synthetic",
-        "config": {"workload": f"config1: {args.gates} independent NAND gate bootstraps per GPU, "
-                               "PARAM_128 (n=630, N=1024, l=2, Bg=2^9, t=8, gamma=2)",
-                   "gates_per_gpu": args.gates},
-        "cpu_baseline": {"value": value, "unit": "gates/s", "cores": cores, "kind": kind,
-                         "sample": sample},
+        "vs_baseline": None, "dtype": "u64 (Goldilocks NTT)" if cpu.kind == "reference" else "u64 (port)",
+        "data": "synthetic: keygen(PARAM_128, seed=7) + SURVEY Appendix A config-1 inputs",
+        "config": config_dict(args.gates, args.gpus),
+        "cpu_baseline": {"value": value, "unit": "gates/s", "cores": cpu.cores, "kind": cpu.kind,
+                         "sample": cpu.sample()},
         "e2e": {"value": value, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -448,15 +540,32 @@ def run_ours(args):
     if not args.no_netlist and ws == 1:
         netlist = config2_latency(ks, P, eng)
 
-    # ---- CPU baseline (oracle port), rank 0 at N=1 only --------------------
-    cpu = None
+    # ---- netlists sharded over the GPUs (config 4; config 5 at N = 8) --------
+    sharded = None
+    if not args.no_netlist and args.sharded != "none":
+        which = ([] if ws == 1 else ["config4"] + (["config5"] if ws == 8 else [])) \
+            if args.sharded == "auto" else [x for x in args.sharded.split(",") if x]
+        if which:
+            sharded = {name: netlist_sharded(name, ks, P, dist, rank, ws) for name in which}
+
+    # ---- CPU baseline: the unmodified reference, rank 0 at N=1 only ---------
+    cpu = cpu_c2 = cpu_c345 = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        model, cores = _cpu_info()
-        ref_out, dt = cpu_oracle_run(P, ks, A, B, cores)
-        cpu = {"value": G / dt, "unit": "gates/s", "cores": cores, "kind": "port",
-               "sample": f"full config-1 batch ({G} NAND bootstraps), oracle/gw_oracle.c "
-                         f"on {cores} threads of {model}; {dt:.2f} s",
+        ref = CpuReference(G)
+        ref.step()                                  # numba JIT warm (cached in NUMBA_CACHE_DIR)
+        times, ref_out = [], None
+        for _ in range(2):
+            ref_out, dt = ref.step()
+            times.append(dt)
+        dt = statistics.median(times)
+        cpu = {"value": G / dt, "unit": "gates/s", "cores": ref.cores, "kind": ref.kind,
+               "sample": ref.sample() + f"; median of {len(times)} steps, {dt:.2f} s per step",
                "bit_exact_vs_gpu": bool(np.array_equal(ref_out, res))}
+        if not args.no_cpu_netlists:
+            # one worker's per-bootstrap time: each of the K workers ran ceil(G / K) bootstraps
+            per_boot = dt / -(-G // ref.cores)
+            cpu_c2 = ref.config2()
+            cpu_c345 = ref.extrapolated_netlists(per_boot)
 
     if rank == 0:
         line = {
@@ -464,11 +573,7 @@ def run_ours(args):
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: keygen(PARAM_128, seed=7) + SURVEY Appendix A config-1 inputs",
-            "config": {"workload": f"config1: {G} independent NAND gate bootstraps per GPU, "
-                                   "PARAM_128 (n=630, N=1024, l=2, Bg=2^9, t=8, gamma=2)",
-                       "gates_per_gpu": G, "bootstraps_per_gate": 1,
-                       "l2": "flushed (512 MB write) between timed steps",
-                       "parallelism": f"dp{ws} (independent gate batches)"},
+            "config": config_dict(G, ws),
             "e2e": {"value": G * ws / e2e_s, "unit": "gates/s",
                     "h2d_bytes_per_step": 2 * G * W * 4, "d2h_bytes_per_step": G * W * 4,
                     "app_latency_s": e2e_s, "api": "paper_2306_11006_b200.cggi.eval_gate_batch"},
@@ -476,6 +581,9 @@ def run_ours(args):
             "roofline": roofline,
             "cpu_baseline": cpu,
             "app_latency_config2": netlist,
+            "app_latency_config2_cpu": cpu_c2,
+            "cpu_netlists_extrapolated": cpu_c345,
+            "netlists_sharded": sharded,
             "throughput_wide_level": wide,
             "param110": p110,
             "clocks": clk.summary(),
@@ -487,10 +595,91 @@ def run_ours(args):
     return 0
 
 
+NETLIST_SEEDS = {"config3": 3, "config4": 4, "config5": 5}
+
+
+def netlist_sharded(name, ks, P, dist, rank, ws):
+    """One BASELINE netlist config evaluated with its levels sharded over the
+    ws GPUs (runtime.evaluate -> exchange.evaluate_distributed: the
+    reference's per-opcode split of every level, scheduler.py:133-157, and the
+    NCCL point-to-point wire exchange).  App latency = host rows in -> host
+    rows out on every rank, max over ranks."""
+    import hashlib
+    import torch
+    from paper_2306_11006_b200 import circuit as C
+    from paper_2306_11006_b200 import netlists as NL
+    from paper_2306_11006_b200.cggi import decrypt_rows, encrypt_bits
+    from paper_2306_11006_b200.rng import SeededRng
+    from paper_2306_11006_b200.runtime import _cached_plan, evaluate
+    from paper_2306_11006_b200.scheduler import bootstraps_of, build_schedule
+    gen = {"config3": lambda: NL.gen_dot_product(500), "config4": lambda: NL.gen_fc_layer(256, 30),
+           "config5": lambda: NL.gen_matmul_sigmoid(10)}[name]
+    t = time.monotonic()
+    c = gen()
+    prep = {"generate_s": time.monotonic() - t}
+    t = time.monotonic()
+    sched = build_schedule(c, ws)
+    prep["schedule_s"] = time.monotonic() - t
+    t = time.monotonic()
+    _cached_plan(c, sched, *((None, None) if ws == 1 else (rank, ws)))
+    prep["plan_compile_s"] = time.monotonic() - t
+    seed = NETLIST_SEEDS[name]
+    rng = np.random.default_rng(seed)
+    bits = {p.name: rng.integers(0, 2, p.width).astype(np.uint8) for p in c.inputs}
+    srng = SeededRng(1000 * seed)
+    inputs = {p.name: encrypt_bits(P, ks.lwe_sk, bits[p.name], srng) for p in c.inputs}
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.monotonic()
+    outs, met = evaluate(c, sched, inputs, ks)
+    torch.cuda.synchronize()
+    app = time.monotonic() - t0
+    if dist is not None:
+        tl = torch.tensor([app], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tl, op=dist.ReduceOp.MAX)
+        app = float(tl.item())
+    h = hashlib.sha256()
+    for p in c.outputs:
+        h.update(np.ascontiguousarray(outs[p.name]).tobytes())
+    ok = None
+    if rank == 0:
+        plain = C.simulate_plain_bits(c, {k: v[:, None] for k, v in bits.items()})
+        ok = all(np.array_equal(decrypt_rows(ks.lwe_sk, outs[k]), plain[k][:, 0]) for k in plain)
+    nb = bootstraps_of(sched)
+    return {"gates": len(c.gates), "bootstraps": nb, "levels": len(sched.waves), "n_gpus": ws,
+            "app_latency_s": app, "gates_per_s": len(c.gates) / app, "bootstraps_per_s": nb / app,
+            "device_time_s": met.device_time_seconds,
+            "exchange_bytes": getattr(met, "exchange_bytes", 0), "transport": getattr(met, "transport", "local"),
+            "output_digest": h.hexdigest()[:16], "decrypt_ok": ok, "host_prep": prep,
+            "seeds": f"default_rng({seed}) bits, SeededRng({1000 * seed}) encryption, keygen(PARAM_128, 7)"}
+
+
+def _self_launch(args) -> int:
+    """--gpus N without torchrun: re-run this script under torch.distributed.run
+    (one process per GPU, 127.0.0.1 rendezvous), exactly as the driver does."""
+    import socket
+    import subprocess
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = _args()
     if args.impl == "reference":
         return run_reference(args)
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is None and args.gpus > 1:
+        return _self_launch(args)
+    if int(ws_env or 1) != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}: one process per GPU required\n")
+        return 2
+    if args.gpus > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")   # the driver checks the communicator's rank count
     return run_ours(args)
 
 

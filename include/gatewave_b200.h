@@ -126,22 +126,42 @@ int gw_plan_destroy(gw_ctx* ctx, gw_plan* plan);
 
 /* Multi-GPU wire exchange between levels (replaces the reference's per-wave
  * WireStore hand-off, runtime.py:166-190, for one process per GPU; SURVEY.md
- * §8(b) gw_exchange_enqueue).  The static plan lists, per level and rank, the
- * wire ids that rank produces and another rank reads later (or that are
- * circuit outputs): ids[offsets[level*world + q] .. offsets[level*world + q + 1]).
- * pack copies this rank's rows of a level into a contiguous device buffer of
- * `pad` rows (the per-level maximum, gw_xplan_pad); the caller's collective
- * (an all-gather over NCCL / NVLink) produces world x pad rows; unpack
- * scatters the other ranks' rows into the wire store.  Both only enqueue on
- * the context stream, so levels, exchanges and the collective stay
- * stream-ordered with no host synchronisation. */
+ * §8(b) gw_exchange_enqueue).  Point-to-point plan: counts[(level*world +
+ * src)*world + dst] is the number of wires rank src produces at `level` that
+ * rank dst needs (reads in a later level, or circuit outputs); ids lists them
+ * in (level, src, dst) order.  Every rank passes the same arrays and keeps its
+ * own sends and receives; the plan owns device staging buffers.
+ * gw_exchange_enqueue packs this rank's rows, runs one grouped ncclSend /
+ * ncclRecv per peer (NCCL over NVLink / NVSwitch, only the rows each peer
+ * reads) and scatters the received rows into the wire store -- all enqueued on
+ * the context stream, no host synchronisation.  nccl_comm is an ncclComm_t
+ * (NULL: the context's own, from gw_nccl_init).  libnccl.so.2 is bound at run
+ * time (GATEWAVE_NCCL_LIB, else the copy already loaded, else the system's).
+ * pack / unpack / peer_rows / buffers expose the same steps for a caller that
+ * moves the staged rows itself (e.g. gloo on CPU). */
 typedef struct gw_xplan gw_xplan;
-int gw_xplan_create(gw_ctx* ctx, int64_t n_levels, int32_t world, const int64_t* offsets, const int64_t* ids,
-                    gw_xplan** out);
-int gw_xplan_pad(gw_ctx* ctx, const gw_xplan* plan, int64_t level, int64_t* pad);
-int gw_exchange_pack(gw_ctx* ctx, const gw_xplan* plan, int64_t level, int32_t rank, uint32_t* d_send);
-int gw_exchange_unpack(gw_ctx* ctx, const gw_xplan* plan, int64_t level, int32_t rank, const uint32_t* d_recv);
+int gw_xplan_create(gw_ctx* ctx, int64_t n_levels, int32_t world, int32_t rank, const int64_t* counts,
+                    const int64_t* ids, gw_xplan** out);
+int gw_xplan_peer_rows(gw_ctx* ctx, const gw_xplan* plan, int64_t level, int64_t* send_rows /* [world] */,
+                       int64_t* recv_rows /* [world] */);
+int gw_xplan_buffers(gw_ctx* ctx, const gw_xplan* plan, void** d_send, void** d_recv);
+int gw_exchange_pack(gw_ctx* ctx, const gw_xplan* plan, int64_t level, uint32_t* d_send /* NULL: plan buffer */);
+int gw_exchange_unpack(gw_ctx* ctx, const gw_xplan* plan, int64_t level, const uint32_t* d_recv /* NULL: plan buffer */);
+int gw_exchange_enqueue(gw_ctx* ctx, const gw_xplan* plan, int64_t level, void* nccl_comm);
 int gw_xplan_destroy(gw_ctx* ctx, gw_xplan* plan);
+/* NCCL bootstrap: version (> 0) when libnccl is usable, else 0 and the reason in `why`. */
+int gw_nccl_available(char* why, int64_t why_len);
+int gw_nccl_unique_id(char* out /* 128 bytes, ncclUniqueId */);
+int gw_nccl_init(gw_ctx* ctx, int32_t world, int32_t rank, const char* unique_id /* 128 bytes */);
+
+/* Device timeline: event marks on the context stream, read after one sync:
+ * ms[k] = time between mark k and mark k+1.  gw_plan_run_timed runs levels
+ * [first, last) with a mark at every level boundary and returns the device
+ * time of each level after a single host synchronisation. */
+int gw_timeline_reset(gw_ctx* ctx);
+int gw_timeline_mark(gw_ctx* ctx);
+int gw_timeline_read(gw_ctx* ctx, float* ms, int64_t cap, int64_t* count);
+int gw_plan_run_timed(gw_ctx* ctx, gw_plan* plan, int64_t first, int64_t last, float* ms /* last - first */);
 
 /* CUDA-event timer on the context stream (milliseconds between start/stop). */
 int gw_timer_start(gw_ctx* ctx);
@@ -156,6 +176,13 @@ int gw_stage_times(gw_ctx* ctx, double* ms, int64_t* items, int reset);
  * its first gate, phases [forward, fill, barrier A, MAC, inverse, step end];
  * needs GATEWAVE_BR_PROFILE=1 at context creation. */
 int gw_br_phase_cycles(gw_ctx* ctx, long long* out);
+/* Rounding-margin probe (exactness evidence): when on, blind
+ * rotations at N = 1024, l = 2 run a probe build that records the worst
+ * |x - rint(x)| over every FP64 value the inverse transforms round to an
+ * integer; gw_margin_read syncs and returns it (< 0.5 means every rounding
+ * recovered the exact integer). */
+int gw_set_margin_probe(gw_ctx* ctx, int on);
+int gw_margin_read(gw_ctx* ctx, double* worst, int reset);
 /* Number of engine kernel launches issued by this context so far. */
 int gw_launch_count(gw_ctx* ctx, int64_t* count);
 

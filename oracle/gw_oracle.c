@@ -24,32 +24,34 @@ static const uint64_t Q = 0xFFFFFFFF00000001ULL;
 static const uint64_t M32 = 0xFFFFFFFFULL;
 static const uint64_t GENERATOR = 12037493425763644479ULL; /* torus.py:23 */
 
-/* torus.py:74-88 (_mm): 128-bit product folded with 2^64 = 2^32 - 1 (mod Q) */
+/* torus.py:74-88 (_mm): 128-bit product folded with 2^64 = 2^32 - 1 (mod Q).
+ * The 64x64 -> 128 product is assembled from four 32x32 -> 64 partial
+ * products (the reference's LLVM i128 multiply lowers the same way when it
+ * vectorises), so gcc can vectorise the transform loops too. */
 static inline uint64_t mm(uint64_t a, uint64_t b) {
-  u128 p = (u128)a * b;
-  uint64_t lo = (uint64_t)p, hi = (uint64_t)(p >> 64);
-  uint64_t h_hi = hi >> 32, h_lo = hi & M32;
-  /* same arithmetic as the reference, written branch-free (conditional moves) */
+  const uint64_t a0 = a & M32, a1 = a >> 32, b0 = b & M32, b1 = b >> 32;
+  const uint64_t p00 = a0 * b0, p01 = a0 * b1, p10 = a1 * b0, p11 = a1 * b1;
+  const uint64_t mid = (p00 >> 32) + (p01 & M32) + (p10 & M32);
+  const uint64_t lo = (p00 & M32) | (mid << 32);
+  const uint64_t hi = p11 + (p01 >> 32) + (p10 >> 32) + (mid >> 32);
+  const uint64_t h_hi = hi >> 32, h_lo = hi & M32;
   uint64_t t = lo - h_hi;
-  t -= (uint64_t)(lo < h_hi) * M32;
+  t = lo < h_hi ? t - M32 : t;
   uint64_t u = (h_lo << 32) - h_lo;
   uint64_t s = t + u;
-  s += (uint64_t)(s < t) * M32;
-  s -= (uint64_t)(s >= Q) * Q;
-  return s;
+  s = s < t ? s + M32 : s;
+  return s >= Q ? s - Q : s;
 }
 /* torus.py:91-98 (_ma) */
 static inline uint64_t ma(uint64_t a, uint64_t b) {
   uint64_t s = a + b;
-  s += (uint64_t)(s < a) * M32;
-  s -= (uint64_t)(s >= Q) * Q;
-  return s;
+  s = s < a ? s + M32 : s;
+  return s >= Q ? s - Q : s;
 }
 /* torus.py:101-106 (_ms) */
 static inline uint64_t ms(uint64_t a, uint64_t b) {
   uint64_t d = a - b;
-  d -= (uint64_t)(a < b) * M32;
-  return d;
+  return a < b ? d - M32 : d;
 }
 
 static uint64_t powmod(uint64_t b, uint64_t e) {

@@ -29,6 +29,20 @@ def build() -> str:
     return _LIB_PATH
 
 
+def use_native() -> str:
+    """Rebuild for THIS host's CPU (-march=native: AVX-512 vectorises the
+    transform loops, ~2x) and load that copy.  For the CPU-baseline timings,
+    which run on the GPU box's host; the portable build stays the test copy."""
+    global _lib, _LIB_PATH
+    out = os.path.join(_HERE, "liboracle_native.so")
+    subprocess.run(["gcc", "-O3", "-march=native", "-pthread", "-fPIC", "-std=c11", "-shared", "-o", out,
+                    os.path.join(_HERE, "gw_oracle.c")], check=True)
+    _LIB_PATH = out
+    _lib = None
+    lib()
+    return out
+
+
 def lib():
     global _lib
     if _lib is None:

@@ -28,6 +28,9 @@ struct BrArgs {
   int gates_per_cta;
   long long* prof;       // optional per-phase cycle counters (debug; nullptr = off)
   int ablate;            // debug timing ablations (0 = exact kernel); see br_tmem.cuh
+  // rounding-margin probe (gw_set_margin_probe): max |x - rint(x)| over every
+  // FP64 value the inverse transforms round, as the bits of a positive double
+  unsigned long long* margin = nullptr;
 };
 
 // Bootstrapping key, FFT domain: [i][c][h][s][r][lane] complex, scaled by 1/M.

@@ -137,7 +137,9 @@ __device__ __forceinline__ void tm_cp_128x256b(uint32_t taddr, uint64_t desc) {
 //
 // KM = key streaming mode: 0 LDG by the compute warps, 1 TMA by warp 0, 2 four
 // dedicated loader warps (one per TMEM sub-partition; GC = 1 only).
-template <int GC, int KM>
+// PROBE: rounding-margin probe build (worst |x - rint(x)| before every rounding
+// of the inverse transform) -- the exactness evidence.
+template <int GC, int KM, bool PROBE = false>
 __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rotate_v3(BrArgs a) {
   constexpr bool TMA = KM == 1, LDR = KM == 2;
   static_assert(!LDR || GC <= 3, "loader warps need registers the compute warps can spare");
@@ -384,6 +386,7 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
   if (kStagger && gl >= 1) mbar_wait(&go_bar[gl - 1], 0);
   uint32_t a_next = __ldg(lin_g);
   uint32_t sink = 0;  // GW_ABL & 8 only
+  double worst = 0.0;  // PROBE only
   for (int i = 0; i < a.n; ++i) {
     const int cur = i & 1, nxt = cur ^ 1;
     const int sn = kRing ? (sc + 4 >= V3::RING ? sc + 4 - V3::RING : sc + 4) : 4 - sc;  // slot base of step i+1
@@ -550,6 +553,7 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
         for (int m1 = 0; m1 < P; ++m1) {
           const double2 v = m1 == 0 ? x[0] : cmulc(x[m1], c_root64[G::CSTEP * m1]);
           const uint32_t j = (uint32_t)(L * m1 + l);
+          if constexpr (PROBE) worst = fmax(worst, fmax(fabs(v.x - rint(v.x)), fabs(v.y - rint(v.y))));
 #if GW_ABL & 8
           sink ^= (round_mod32(v.x) << shift) + round_mod32(v.y);
           (void)j;
@@ -584,6 +588,11 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
   if (active) atomicXor(acc_g, sink);
 #endif
   (void)sink;
+  if constexpr (PROBE) {
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, d));
+    if (lane == 0 && active && a.margin) atomicMax(a.margin, (unsigned long long)__double_as_longlong(worst));
+  }
   if (prof)
     for (int ph = 0; ph < 6; ++ph) a.prof[o * 6 + ph] = pt_[ph];
   if (active && o < 2) {

@@ -6,13 +6,18 @@
 //   k_lin -> k_blind_rotate -> k_zero_units -> k_keyswitch -> k_cheap
 // All launches go to the context stream; only the host-pointer entry points
 // synchronise (they must hand results back to the caller).
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/gatewave_b200.h"
@@ -36,6 +41,7 @@ struct BatchDesc {
 struct gw_ctx {
   int device = 0;
   int sm_count = 148;
+  int max_smem = 0;  // cudaDevAttrMaxSharedMemoryPerBlockOptin, cached
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   gw_params p{};
@@ -69,6 +75,7 @@ struct gw_ctx {
   size_t desc_cap = 0;  // bytes
   void* desc_host = nullptr;  // pinned
   size_t desc_host_cap = 0;
+  cudaEvent_t desc_copied = nullptr;  // the last H2D copy out of desc_host
   // wire store
   uint32_t* wires = nullptr;
   int64_t wire_slots = 0;
@@ -90,6 +97,10 @@ struct gw_ctx {
   int br_gc = 0;  // v3 gates per CTA override (GATEWAVE_BR_GC, measurement only; 0 = by batch size)
   bool br_gc1_tma = false;
   bool br_ldr = true;  // loader warps at GC = 2, 3 (GATEWAVE_BR_LDR=0: LDG by the compute warps)  // GATEWAVE_BR_GC1=tma: one-gate CTAs stage the key through shared memory
+  std::vector<cudaEvent_t> marks;  // device timeline (gw_timeline_*)
+  void* nccl = nullptr;            // ncclComm_t owned by the context (gw_nccl_init)
+  unsigned long long* margin = nullptr;  // rounding-margin probe accumulator (gw_set_margin_probe)
+  int nccl_world = 0, nccl_rank = 0;
   std::string err;
 };
 
@@ -102,6 +113,7 @@ struct gw_plan {
   KsUnit* units = nullptr;
   CheapUnit* cheap = nullptr;
   int max_jobs = 0;
+  int64_t max_wire = -1;  // highest wire id the plan touches (checked against the store at run time)
 };
 
 namespace {
@@ -168,6 +180,27 @@ int ensure_desc(gw_ctx* c, size_t bytes) {
   return GW_OK;
 }
 
+// cudaFuncSetAttribute / cudaDeviceGetAttribute cost microseconds per call: the
+// dynamic shared-memory size set on a kernel and the device's opt-in limit are
+// cached per (device, kernel).
+int max_smem_optin(gw_ctx* c) {
+  if (c->max_smem <= 0) cudaDeviceGetAttribute(&c->max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+  return c->max_smem;
+}
+
+template <typename K>
+int set_smem(gw_ctx* c, K* kern, size_t bytes) {
+  static std::map<std::pair<int, const void*>, size_t> applied;
+  static std::mutex mtx;
+  std::lock_guard<std::mutex> lk(mtx);
+  const auto key = std::make_pair(c->device, (const void*)kern);
+  auto it = applied.find(key);
+  if (it != applied.end() && it->second >= bytes) return GW_OK;
+  GW_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  applied[key] = bytes;
+  return GW_OK;
+}
+
 // Host twiddle tables, long double -> correctly rounded-ish doubles.
 void host_tables(int logn, std::vector<double2>& out) {
   const int N = 1 << logn, M = N / 2;
@@ -224,14 +257,12 @@ int launch_br_t(gw_ctx* c, const BrArgs& a0) {
   int gc = (int)((a.B + c->sm_count - 1) / c->sm_count);
   if (gc < 1) gc = 1;
   if (gc > 4) gc = 4;
-  int max_smem = 0;
-  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+  const int max_smem = max_smem_optin(c);
   while (gc > 1 && BrSmem<LOGN, LEV>::bytes(gc, a.n) > (size_t)max_smem) --gc;
   const size_t smem = BrSmem<LOGN, LEV>::bytes(gc, a.n);
   if (smem > (size_t)max_smem)
     return fail(c, GW_ERR_PARAM, "LWE dimension too large for the on-chip blind rotation");
-  GW_CUDA(c, cudaFuncSetAttribute(k_blind_rotate<LOGN, LEV>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (int rc = set_smem(c, k_blind_rotate<LOGN, LEV>, smem)) return rc;
   a.gates_per_cta = gc;
   const int grid = (a.B + gc - 1) / gc;
   k_blind_rotate<LOGN, LEV><<<grid, 64 * gc, smem, c->stream>>>(a);
@@ -244,8 +275,7 @@ int launch_tm_g(gw_ctx* c, const BrArgs& a0, int max_smem) {
   BrArgs a = a0;
   const size_t smem = TmGeo<LOGN, LEV>::smem_bytes(GC, a.n);
   if (smem > (size_t)max_smem) return 1;  // caller falls back
-  GW_CUDA(c, cudaFuncSetAttribute(k_blind_rotate_tm<LOGN, LEV, GC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
+  if (int rc = set_smem(c, k_blind_rotate_tm<LOGN, LEV, GC>, smem)) return rc;
   a.gates_per_cta = GC;
   const int grid = (a.B + GC - 1) / GC;
   k_blind_rotate_tm<LOGN, LEV, GC><<<grid, 128 * GC, smem, c->stream>>>(a);
@@ -256,8 +286,7 @@ int launch_tm_g(gw_ctx* c, const BrArgs& a0, int max_smem) {
 // TMEM 4-warp kernel: one CTA per SM (it owns the TMEM), GC gates per CTA.
 template <int LOGN, int LEV>
 int launch_tm(gw_ctx* c, const BrArgs& a) {
-  int max_smem = 0;
-  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+  const int max_smem = max_smem_optin(c);
   const int per_sm = (int)((a.B + c->sm_count - 1) / c->sm_count);
   int rc = 1;
   if (per_sm >= 3) rc = launch_tm_g<LOGN, LEV, 4>(c, a, max_smem);
@@ -267,16 +296,16 @@ int launch_tm(gw_ctx* c, const BrArgs& a) {
   return rc;
 }
 
-template <int GC, int KM>
+template <int GC, int KM, bool PROBE = false>
 int launch_v3_g(gw_ctx* c, const BrArgs& a0) {
   BrArgs a = a0;
   a.bk = c->bk_v3;
+  a.margin = PROBE ? c->margin : nullptr;
   const size_t smem = V3::smem_bytes(GC, KM == 1);
-  GW_CUDA(c, cudaFuncSetAttribute(k_blind_rotate_v3<GC, KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
+  if (int rc = set_smem(c, k_blind_rotate_v3<GC, KM, PROBE>, smem)) return rc;
   a.gates_per_cta = GC;
   const int grid = (a.B + GC - 1) / GC;
-  k_blind_rotate_v3<GC, KM><<<grid, 128 * GC + (KM == 2 ? 128 : 0), smem, c->stream>>>(a);
+  k_blind_rotate_v3<GC, KM, PROBE><<<grid, 128 * GC + (KM == 2 ? 128 : 0), smem, c->stream>>>(a);
   GW_LAUNCHED(c);
   return GW_OK;
 }
@@ -298,6 +327,11 @@ int launch_v3(gw_ctx* c, const BrArgs& a) {
     }
   }
   if (c->br_gc > 0) gc = c->br_gc;
+  if (c->margin) {  // rounding-margin probe build: loader-warp variants only
+    if (gc >= 3) return launch_v3_g<3, 2, true>(c, a);
+    if (gc == 2) return launch_v3_g<2, 2, true>(c, a);
+    return launch_v3_g<1, 2, true>(c, a);
+  }
   if (gc >= 4) return launch_v3_g<4, 0>(c, a);
   if (gc == 3) return c->br_ldr ? launch_v3_g<3, 2>(c, a) : launch_v3_g<3, 0>(c, a);
   if (gc == 2) return c->br_ldr ? launch_v3_g<2, 2>(c, a) : launch_v3_g<2, 0>(c, a);
@@ -358,7 +392,7 @@ int launch_ks(gw_ctx* c, const uint32_t* acc, const KsUnit* units, int U, uint32
   if (U <= 0) return GW_OK;
   const int N = c->p.N, W = c->p.n + 1;
   {
-    dim3 grid((W + 255) / 256, U);
+    dim3 grid((W + 255) / 256, grid_rows(U));
     k_zero_units<<<grid, 256, 0, c->stream>>>(units, U, out, out_stride, W);
     GW_LAUNCHED(c);
   }
@@ -396,7 +430,7 @@ int launch_ks(gw_ctx* c, const uint32_t* acc, const KsUnit* units, int U, uint32
     const size_t smem = (size_t)KT_STAGES * (KT_A_BYTES + KT_B_BYTES) + 256;
     dim3 grid(mt, c->kt_ntiles, splits);
     auto go = [&](auto kern) -> int {
-      GW_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      if (int rc = set_smem(c, kern, smem)) return rc;
       kern<<<grid, KT_THREADS, smem, c->stream>>>(k);
       GW_LAUNCHED(c);
       return GW_OK;
@@ -439,7 +473,7 @@ int launch_ks(gw_ctx* c, const uint32_t* acc, const KsUnit* units, int U, uint32
 int launch_lin(gw_ctx* c, const uint32_t* rows, int64_t stride, const LinJob* jobs, int J) {
   if (J <= 0) return GW_OK;
   const int W = c->p.n + 1;
-  dim3 grid((W + 255) / 256, J);
+  dim3 grid((W + 255) / 256, grid_rows(J));
   k_lin<<<grid, 256, 0, c->stream>>>(rows, stride, jobs, J, W, c->p.mu, c->lin, c->Wp);
   GW_LAUNCHED(c);
   return GW_OK;
@@ -449,7 +483,7 @@ int launch_cheap(gw_ctx* c, const uint32_t* src, int64_t src_stride, const Cheap
                  uint32_t* dst, int64_t dst_stride) {
   if (C <= 0) return GW_OK;
   const int W = c->p.n + 1;
-  dim3 grid((W + 255) / 256, C);
+  dim3 grid((W + 255) / 256, grid_rows(C));
   k_cheap<<<grid, 256, 0, c->stream>>>(src, src_stride, units, C, W, c->p.mu, dst, dst_stride);
   GW_LAUNCHED(c);
   return GW_OK;
@@ -569,14 +603,17 @@ int upload_desc(gw_ctx* c, const std::vector<LinJob>& jobs, const std::vector<Ks
                bc = cheap.size() * sizeof(CheapUnit);
   const size_t total = bj + bu + bc;
   int rc;
-  // the pinned staging buffer may still feed an earlier async copy
-  GW_CUDA(c, cudaStreamSynchronize(c->stream));
+  // the pinned staging buffer may still feed the previous async copy: wait for
+  // that copy only (an event), not for the whole stream
+  if (c->desc_copied) GW_CUDA(c, cudaEventSynchronize(c->desc_copied));
   if ((rc = ensure_desc(c, total))) return rc;
   char* h = (char*)c->desc_host;
   if (bj) memcpy(h, jobs.data(), bj);
   if (bu) memcpy(h + bj, units.data(), bu);
   if (bc) memcpy(h + bj + bu, cheap.data(), bc);
   GW_CUDA(c, cudaMemcpyAsync(c->desc, h, total, cudaMemcpyHostToDevice, c->stream));
+  if (!c->desc_copied) GW_CUDA(c, cudaEventCreateWithFlags(&c->desc_copied, cudaEventDisableTiming));
+  GW_CUDA(c, cudaEventRecord(c->desc_copied, c->stream));
   char* d = (char*)c->desc;
   *dj = (LinJob*)d;
   *du = (KsUnit*)(d + bj);
@@ -584,6 +621,63 @@ int upload_desc(gw_ctx* c, const std::vector<LinJob>& jobs, const std::vector<Ks
   return GW_OK;
 }
 
+}  // namespace
+
+namespace {
+// libnccl is bound at run time (dlopen) so the engine has no link-time NCCL
+// dependency: the one torch already loaded when present, else the system's.
+struct NcclApi {
+  bool tried = false, ok = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*GetVersion)(int*) = nullptr;
+};
+std::mutex g_nccl_mtx;
+NcclApi g_nccl;
+
+const NcclApi& nccl_api() {
+  std::lock_guard<std::mutex> lk(g_nccl_mtx);
+  if (g_nccl.tried) return g_nccl;
+  g_nccl.tried = true;
+  void* h = nullptr;
+  if (const char* p = getenv("GATEWAVE_NCCL_LIB")) h = dlopen(p, RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);  // already in the process (torch)
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    g_nccl.why = std::string("libnccl.so.2 not found: ") + dlerror();
+    return g_nccl;
+  }
+  bool ok = true;
+  auto sym = [&](auto& fn, const char* name) {
+    fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+    if (!fn) ok = false;
+  };
+  sym(g_nccl.GetUniqueId, "ncclGetUniqueId");
+  sym(g_nccl.CommInitRank, "ncclCommInitRank");
+  sym(g_nccl.CommDestroy, "ncclCommDestroy");
+  sym(g_nccl.Send, "ncclSend");
+  sym(g_nccl.Recv, "ncclRecv");
+  sym(g_nccl.GroupStart, "ncclGroupStart");
+  sym(g_nccl.GroupEnd, "ncclGroupEnd");
+  sym(g_nccl.GetErrorString, "ncclGetErrorString");
+  sym(g_nccl.GetVersion, "ncclGetVersion");
+  g_nccl.ok = ok;
+  if (!ok) g_nccl.why = "libnccl.so.2 lacks a required symbol";
+  return g_nccl;
+}
+
+#define GW_NCCL(ctx, api, expr)                                                                   \
+  do {                                                                                            \
+    ncclResult_t r_ = (expr);                                                                     \
+    if (r_ != ncclSuccess) return fail((ctx), GW_ERR_CUDA, std::string(#expr) + ": " + (api).GetErrorString(r_)); \
+  } while (0)
 }  // namespace
 
 // ============================================================================
@@ -661,6 +755,7 @@ int gw_destroy(gw_ctx* c) {
   cudaFree(c->kimg);
   cudaFree(c->ks_ut);
   cudaFree(c->br_prof);
+  cudaFree(c->margin);
   cudaFree(c->tables);
   cudaFree(c->tv_dev);
   cudaFree(c->lin);
@@ -675,9 +770,15 @@ int gw_destroy(gw_ctx* c) {
       cudaEventDestroy(pr.first);
       cudaEventDestroy(pr.second);
     }
+  for (auto e : c->marks) cudaEventDestroy(e);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->nccl) {
+    const NcclApi& api = nccl_api();
+    if (api.ok) api.CommDestroy((ncclComm_t)c->nccl);
+  }
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->desc_copied) cudaEventDestroy(c->desc_copied);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return GW_OK;
@@ -723,8 +824,10 @@ int gw_set_params(gw_ctx* c, const gw_params* p) {
     return fail(c, GW_ERR_PARAM, "ring dimension not supported by the B200 engine (64, 256, 1024)");
   if (p->l > 3) return fail(c, GW_ERR_PARAM, "gadget levels > 3 not supported by the B200 engine");
   if (p->bg_bits > 16) return fail(c, GW_ERR_PARAM, "gadget base > 2^16 not supported by the B200 engine");
-  // |coefficient| <= 2l * N * 2^(Bg-1) * 2^15 must stay <= 2^40 for the FFT bound
-  if (std::log2(2.0 * p->l) + logn + (p->bg_bits - 1) + 15 > 40.0)
+  // |coefficient| <= 2l * N * 2^(Bg-1) * 2^15 must stay <= 2^36: the largest
+  // magnitude whose rounding margin is measured (Bg = 10, l = 2, N = 1024:
+  // tests/test_gpu_margin.py); PARAM_128 / PARAM_110 sit at 2^35
+  if (std::log2(2.0 * p->l) + logn + (p->bg_bits - 1) + 15 > 36.0 + 1e-9)
     return fail(c, GW_ERR_PARAM, "parameters outside the exact FP64 convolution envelope");
   if (p->ks_levels * p->ks_base_bits > 31)
     return fail(c, GW_ERR_PARAM, "keyswitch precision t*gamma > 31 not supported by the B200 engine");
@@ -734,8 +837,16 @@ int gw_set_params(gw_ctx* c, const gw_params* p) {
   c->logn = logn;
   c->Wp = (p->n + 1 + 3) & ~3;
   c->have_params = true;
-  if (!same) c->have_keys = c->have_bk = c->have_ksk = false;
   cudaSetDevice(c->device);
+  if (!same) {
+    c->have_keys = c->have_bk = c->have_ksk = false;
+    // cached gate-batch descriptors carry mu (MUX units): drop them
+    if (!c->batch_desc.empty()) {
+      GW_CUDA(c, cudaStreamSynchronize(c->stream));
+      for (auto& kv : c->batch_desc) cudaFree(kv.second.mem);
+      c->batch_desc.clear();
+    }
+  }
   // tables + default test vector (cggi.py:712-713: a = 0, b = mu)
   std::vector<double2> t;
   host_tables(logn, t);
@@ -902,7 +1013,7 @@ int gw_keyswitch(gw_ctx* c, const uint32_t* ext, int64_t B, uint32_t* out) {
   uint32_t* dout = c->io + ext_words;
   GW_CUDA(c, cudaMemcpyAsync(dext, ext, ext_words * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
   {
-    dim3 grid((2 * N + 255) / 256, (unsigned)B);
+    dim3 grid((2 * N + 255) / 256, grid_rows(B));
     k_ext_to_acc<<<grid, 256, 0, c->stream>>>(dext, B, N, c->acc);
     GW_LAUNCHED(c);
   }
@@ -921,45 +1032,59 @@ int gw_keyswitch(gw_ctx* c, const uint32_t* ext, int64_t B, uint32_t* out) {
   return GW_OK;
 }
 
+// Gates per launch set of a homogeneous batch (the same cut as the level plans):
+// whole waves of the blind rotation at 3 and 4 gates per CTA; bounds the
+// scratch (lin rows + accumulators, ~130 MB) however large the batch.
+constexpr int64_t kSegGates = 148 * 12 * 9;
+
 static int eval_stacked(gw_ctx* c, int opcode, const uint32_t* stacked, int64_t in_stride, int arity, int64_t B,
                         uint32_t* d_out, int64_t out_stride) {
-  // Descriptors of a homogeneous batch depend only on (opcode, B): cache them
-  // on the device so repeated batches enqueue without any host round trip.
-  const uint64_t key = ((uint64_t)opcode << 40) | (uint64_t)B;
-  auto it = c->batch_desc.find(key);
-  if (it == c->batch_desc.end()) {
-    std::vector<LinJob> jobs;
-    std::vector<KsUnit> units;
-    std::vector<CheapUnit> cheap;
-    for (int64_t g = 0; g < B; ++g) {
-      const int32_t s0 = arity > 0 ? (int32_t)g : -1;
-      const int32_t s1 = arity > 1 ? (int32_t)(B + g) : -1;
-      const int32_t s2 = arity > 2 ? (int32_t)(2 * B + g) : -1;
-      describe_gate(opcode, s0, s1, s2, (int32_t)g, c->p.mu, jobs, units, cheap);
+  for (int64_t g0 = 0; g0 < B; g0 += kSegGates) {
+    const int64_t S = std::min<int64_t>(kSegGates, B - g0);
+    // Descriptors of a homogeneous segment depend only on (opcode, S, B): cache
+    // them on the device so repeated batches enqueue without any host round trip.
+    // Operand k of gate g is stacked row k*B + g; the segment's rows are reached
+    // by offsetting the base pointers by g0 rows.
+    const uint64_t key = ((uint64_t)opcode << 56) | ((uint64_t)S << 28) | (uint64_t)B;
+    auto it = c->batch_desc.find(key);
+    if (it == c->batch_desc.end()) {
+      std::vector<LinJob> jobs;
+      std::vector<KsUnit> units;
+      std::vector<CheapUnit> cheap;
+      for (int64_t g = 0; g < S; ++g) {
+        const int32_t s0 = arity > 0 ? (int32_t)g : -1;
+        const int32_t s1 = arity > 1 ? (int32_t)(B + g) : -1;
+        const int32_t s2 = arity > 2 ? (int32_t)(2 * B + g) : -1;
+        describe_gate(opcode, s0, s1, s2, (int32_t)g, c->p.mu, jobs, units, cheap);
+      }
+      BatchDesc d;
+      d.J = (int)jobs.size();
+      d.U = (int)units.size();
+      d.C = (int)cheap.size();
+      const size_t bj = jobs.size() * sizeof(LinJob), bu = units.size() * sizeof(KsUnit),
+                   bc = cheap.size() * sizeof(CheapUnit);
+      if (c->batch_desc.size() > 64) {
+        GW_CUDA(c, cudaStreamSynchronize(c->stream));
+        for (auto& kv : c->batch_desc) cudaFree(kv.second.mem);
+        c->batch_desc.clear();
+      }
+      GW_CUDA(c, cudaMalloc(&d.mem, bj + bu + bc + 16));
+      char* m = (char*)d.mem;
+      if (bj) GW_CUDA(c, cudaMemcpy(m, jobs.data(), bj, cudaMemcpyHostToDevice));
+      if (bu) GW_CUDA(c, cudaMemcpy(m + bj, units.data(), bu, cudaMemcpyHostToDevice));
+      if (bc) GW_CUDA(c, cudaMemcpy(m + bj + bu, cheap.data(), bc, cudaMemcpyHostToDevice));
+      d.jobs = (LinJob*)m;
+      d.units = (KsUnit*)(m + bj);
+      d.cheap = (CheapUnit*)(m + bj + bu);
+      it = c->batch_desc.emplace(key, d).first;
     }
-    BatchDesc d;
-    d.J = (int)jobs.size();
-    d.U = (int)units.size();
-    d.C = (int)cheap.size();
-    const size_t bj = jobs.size() * sizeof(LinJob), bu = units.size() * sizeof(KsUnit),
-                 bc = cheap.size() * sizeof(CheapUnit);
-    GW_CUDA(c, cudaMalloc(&d.mem, bj + bu + bc + 16));
-    char* m = (char*)d.mem;
-    if (bj) GW_CUDA(c, cudaMemcpy(m, jobs.data(), bj, cudaMemcpyHostToDevice));
-    if (bu) GW_CUDA(c, cudaMemcpy(m + bj, units.data(), bu, cudaMemcpyHostToDevice));
-    if (bc) GW_CUDA(c, cudaMemcpy(m + bj + bu, cheap.data(), bc, cudaMemcpyHostToDevice));
-    d.jobs = (LinJob*)m;
-    d.units = (KsUnit*)(m + bj);
-    d.cheap = (CheapUnit*)(m + bj + bu);
-    if (c->batch_desc.size() > 64) {
-      GW_CUDA(c, cudaStreamSynchronize(c->stream));
-      for (auto& kv : c->batch_desc) cudaFree(kv.second.mem);
-      c->batch_desc.clear();
-    }
-    it = c->batch_desc.emplace(key, d).first;
+    const BatchDesc& d = it->second;
+    const uint32_t* src = stacked ? stacked + (size_t)g0 * in_stride : nullptr;
+    int rc = run_level(c, src, in_stride, d_out + (size_t)g0 * out_stride, out_stride, d.jobs, d.J, d.units, d.U,
+                       d.cheap, d.C);
+    if (rc) return rc;
   }
-  const BatchDesc& d = it->second;
-  return run_level(c, stacked, in_stride, d_out, out_stride, d.jobs, d.J, d.units, d.U, d.cheap, d.C);
+  return GW_OK;
 }
 
 static int check_batch(gw_ctx* c, int opcode, int arity, int64_t B) {
@@ -1122,7 +1247,6 @@ int gw_plan_create(gw_ctx* c, int64_t n_levels, const int64_t* offs, const int32
   // a level are independent): a segment is one launch set, so scratch memory
   // stays bounded (~1 GB) however wide the level is.  kSegGates is a multiple
   // of 148 SMs x 3 and x 4 gates per CTA, i.e. whole waves of the blind rotation.
-  constexpr int64_t kSegGates = 148 * 12 * 9;  // whole waves at 3 and 4 gates per CTA
   for (int64_t lv = 0; lv < n_levels; ++lv) {
    p->seg_first.push_back((int64_t)p->J.size());
    for (int64_t s0 = offs[lv]; s0 < offs[lv + 1] || s0 == offs[lv]; s0 += kSegGates) {
@@ -1148,6 +1272,8 @@ int gw_plan_create(gw_ctx* c, int64_t n_levels, const int64_t* offs, const int32
         delete p;
         return fail(c, GW_ERR_WIRE, "output wire out of range: " + std::to_string(out_ids[g]));
       }
+      for (int k = 0; k < ar; ++k) p->max_wire = std::max<int64_t>(p->max_wire, s[k]);
+      p->max_wire = std::max<int64_t>(p->max_wire, out_ids[g]);
       describe_gate(op, s[0], s[1], s[2], out_ids[g], c->p.mu, jobs, units, cheap);
     }
     // job indices inside units are level-local
@@ -1186,6 +1312,10 @@ int gw_plan_run_levels(gw_ctx* c, gw_plan* p, int64_t first, int64_t last) {
   if (rc) return rc;
   if (!p) return fail(c, GW_ERR_ARG, "null plan");
   if (!c->wires) return fail(c, GW_ERR_STATE, "wire store not allocated");
+  // the store may have been re-allocated (smaller) since the plan was built
+  if (p->max_wire >= c->wire_slots)
+    return fail(c, GW_ERR_WIRE, "plan references wire " + std::to_string(p->max_wire) + " but the wire store has " +
+                                    std::to_string(c->wire_slots) + " slots");
   if (first < 0) first = 0;
   if (last > p->n_levels) last = p->n_levels;
   if (first >= last) return GW_OK;
@@ -1210,41 +1340,88 @@ int gw_plan_destroy(gw_ctx* c, gw_plan* p) {
   return GW_OK;
 }
 
+// ---- multi-GPU wire exchange: point-to-point plan + native NCCL -------------
+//
+// counts[(level*world + src)*world + dst] = rows rank src produces at `level`
+// that rank dst needs; ids in (level, src, dst) order.  Every rank passes the
+// same arrays and keeps its own sends (src == rank, grouped by dst) and
+// receives (dst == rank, grouped by src).  Send / receive staging buffers are
+// owned by the plan, sized for the widest level.
 struct gw_xplan {
   int64_t n_levels = 0;
-  int world = 1;
-  std::vector<int64_t> offs;  // host copy: (n_levels * world + 1)
-  std::vector<int64_t> pad;   // per level: max rows any rank sends
-  int64_t* d_offs = nullptr;  // device copy of offs
-  int64_t* d_ids = nullptr;
+  int world = 1, rank = 0;
+  std::vector<int64_t> send_cnt, recv_cnt;      // [level][peer]
+  std::vector<int64_t> send_off, recv_off;      // [level]: first row in the device id lists
+  std::vector<int64_t> send_tot, recv_tot;      // [level]
+  int64_t max_send = 0, max_recv = 0;
+  int64_t* d_send_ids = nullptr;
+  int64_t* d_recv_ids = nullptr;
+  uint32_t* d_send = nullptr;
+  uint32_t* d_recv = nullptr;
 };
 
-int gw_xplan_create(gw_ctx* c, int64_t n_levels, int32_t world, const int64_t* offsets, const int64_t* ids,
-                    gw_xplan** out) {
-  if (!c || !out || n_levels < 0 || world < 1 || (n_levels > 0 && !offsets)) return GW_ERR_ARG;
+
+int gw_xplan_create(gw_ctx* c, int64_t n_levels, int32_t world, int32_t rank, const int64_t* counts,
+                    const int64_t* ids, gw_xplan** out) {
+  if (!c || !out || n_levels < 0 || world < 1 || rank < 0 || rank >= world) return GW_ERR_ARG;
   *out = nullptr;
-  const int64_t nl = n_levels * world;
-  if (offsets[0] != 0) return fail(c, GW_ERR_ARG, "exchange offsets must start at 0");
-  for (int64_t k = 0; k < nl; ++k)
-    if (offsets[k + 1] < offsets[k]) return fail(c, GW_ERR_ARG, "exchange offsets must not decrease");
-  const int64_t total = offsets[nl];
+  const int64_t cells = n_levels * world * world;
+  if (cells > 0 && !counts) return GW_ERR_ARG;
+  int64_t total = 0;
+  for (int64_t k = 0; k < cells; ++k) {
+    if (counts[k] < 0) return fail(c, GW_ERR_ARG, "exchange counts must be >= 0");
+    total += counts[k];
+  }
   if (total > 0 && !ids) return GW_ERR_ARG;
   for (int64_t k = 0; k < total; ++k)
     if (ids[k] < 0 || ids[k] >= c->wire_slots)
       return fail(c, GW_ERR_WIRE, "exchange wire id out of range: " + std::to_string(ids[k]));
-  cudaSetDevice(c->device);
   gw_xplan* x = new gw_xplan();
   x->n_levels = n_levels;
   x->world = world;
-  x->offs.assign(offsets, offsets + nl + 1);
-  x->pad.assign(n_levels, 0);
-  for (int64_t L = 0; L < n_levels; ++L)
+  x->rank = rank;
+  std::vector<int64_t> sids, rids;
+  x->send_cnt.assign(n_levels * world, 0);
+  x->recv_cnt.assign(n_levels * world, 0);
+  int64_t pos = 0;
+  for (int64_t L = 0; L < n_levels; ++L) {
+    x->send_off.push_back((int64_t)sids.size());
+    x->recv_off.push_back((int64_t)rids.size());
+    // (src, dst) cells of this level in order; rows of src -> dst are ids[pos .. pos + n)
+    std::vector<std::pair<int64_t, int64_t>> cell(world * world);
     for (int q = 0; q < world; ++q)
-      x->pad[L] = std::max<int64_t>(x->pad[L], offsets[L * world + q + 1] - offsets[L * world + q]);
-  cudaError_t e = cudaMalloc(&x->d_offs, (nl + 1) * sizeof(int64_t));
-  if (e == cudaSuccess) e = cudaMemcpy(x->d_offs, offsets, (nl + 1) * sizeof(int64_t), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess && total > 0) e = cudaMalloc(&x->d_ids, total * sizeof(int64_t));
-  if (e == cudaSuccess && total > 0) e = cudaMemcpy(x->d_ids, ids, total * sizeof(int64_t), cudaMemcpyHostToDevice);
+      for (int r = 0; r < world; ++r) {
+        const int64_t n = counts[(L * world + q) * world + r];
+        cell[q * world + r] = {pos, n};
+        pos += n;
+      }
+    for (int r = 0; r < world; ++r) {  // sends grouped by destination
+      if (r == rank) continue;
+      const auto& cl = cell[rank * world + r];
+      sids.insert(sids.end(), ids + cl.first, ids + cl.first + cl.second);
+      x->send_cnt[L * world + r] = cl.second;
+    }
+    for (int q = 0; q < world; ++q) {  // receives grouped by source
+      if (q == rank) continue;
+      const auto& cl = cell[q * world + rank];
+      rids.insert(rids.end(), ids + cl.first, ids + cl.first + cl.second);
+      x->recv_cnt[L * world + q] = cl.second;
+    }
+    x->send_tot.push_back((int64_t)sids.size() - x->send_off.back());
+    x->recv_tot.push_back((int64_t)rids.size() - x->recv_off.back());
+    x->max_send = std::max(x->max_send, x->send_tot.back());
+    x->max_recv = std::max(x->max_recv, x->recv_tot.back());
+  }
+  cudaSetDevice(c->device);
+  cudaError_t e = cudaSuccess;
+  if (!sids.empty()) e = cudaMalloc(&x->d_send_ids, sids.size() * sizeof(int64_t));
+  if (e == cudaSuccess && !sids.empty())
+    e = cudaMemcpy(x->d_send_ids, sids.data(), sids.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !rids.empty()) e = cudaMalloc(&x->d_recv_ids, rids.size() * sizeof(int64_t));
+  if (e == cudaSuccess && !rids.empty())
+    e = cudaMemcpy(x->d_recv_ids, rids.data(), rids.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && x->max_send) e = cudaMalloc(&x->d_send, (size_t)x->max_send * c->Wp * sizeof(uint32_t));
+  if (e == cudaSuccess && x->max_recv) e = cudaMalloc(&x->d_recv, (size_t)x->max_recv * c->Wp * sizeof(uint32_t));
   if (e != cudaSuccess) {
     gw_xplan_destroy(c, x);
     return fail(c, GW_ERR_CUDA, cudaGetErrorString(e));
@@ -1253,45 +1430,218 @@ int gw_xplan_create(gw_ctx* c, int64_t n_levels, int32_t world, const int64_t* o
   return GW_OK;
 }
 
-int gw_xplan_pad(gw_ctx* c, const gw_xplan* x, int64_t level, int64_t* pad) {
-  if (!c || !x || !pad || level < 0 || level >= x->n_levels) return GW_ERR_ARG;
-  *pad = x->pad[level];
+int gw_xplan_peer_rows(gw_ctx* c, const gw_xplan* x, int64_t level, int64_t* send_rows, int64_t* recv_rows) {
+  if (!c || !x || level < 0 || level >= x->n_levels || !send_rows || !recv_rows) return GW_ERR_ARG;
+  for (int q = 0; q < x->world; ++q) {
+    send_rows[q] = x->send_cnt[level * x->world + q];
+    recv_rows[q] = x->recv_cnt[level * x->world + q];
+  }
   return GW_OK;
 }
 
-int gw_exchange_pack(gw_ctx* c, const gw_xplan* x, int64_t level, int32_t rank, uint32_t* d_send) {
-  if (!c || !x || level < 0 || level >= x->n_levels || rank < 0 || rank >= x->world) return GW_ERR_ARG;
+int gw_xplan_buffers(gw_ctx* c, const gw_xplan* x, void** d_send, void** d_recv) {
+  if (!c || !x || !d_send || !d_recv) return GW_ERR_ARG;
+  *d_send = x->d_send;
+  *d_recv = x->d_recv;
+  return GW_OK;
+}
+
+int gw_exchange_pack(gw_ctx* c, const gw_xplan* x, int64_t level, uint32_t* d_send) {
+  if (!c || !x || level < 0 || level >= x->n_levels) return GW_ERR_ARG;
   if (!c->wires) return fail(c, GW_ERR_STATE, "wire store not allocated");
-  const int64_t k0 = x->offs[level * x->world + rank], n = x->offs[level * x->world + rank + 1] - k0;
+  const int64_t n = x->send_tot[level];
   if (n == 0) return GW_OK;
-  if (!d_send) return GW_ERR_ARG;
+  if (!d_send) d_send = x->d_send;
   cudaSetDevice(c->device);
-  dim3 grid(1, (unsigned)n);
-  k_xpack<<<grid, 160, 0, c->stream>>>(c->wires, c->Wp, x->d_ids + k0, n, d_send, c->Wp);
+  k_xpack<<<dim3(1, grid_rows(n)), 160, 0, c->stream>>>(c->wires, c->Wp, x->d_send_ids + x->send_off[level], n,
+                                                        d_send, c->Wp);
   GW_LAUNCHED(c);
   return GW_OK;
 }
 
-int gw_exchange_unpack(gw_ctx* c, const gw_xplan* x, int64_t level, int32_t rank, const uint32_t* d_recv) {
-  if (!c || !x || level < 0 || level >= x->n_levels || rank < 0 || rank >= x->world) return GW_ERR_ARG;
+int gw_exchange_unpack(gw_ctx* c, const gw_xplan* x, int64_t level, const uint32_t* d_recv) {
+  if (!c || !x || level < 0 || level >= x->n_levels) return GW_ERR_ARG;
   if (!c->wires) return fail(c, GW_ERR_STATE, "wire store not allocated");
-  const int64_t pad = x->pad[level];
-  if (pad == 0 || x->world == 1) return GW_OK;
-  if (!d_recv) return GW_ERR_ARG;
+  const int64_t n = x->recv_tot[level];
+  if (n == 0) return GW_OK;
+  if (!d_recv) d_recv = x->d_recv;
   cudaSetDevice(c->device);
-  dim3 grid(1, (unsigned)pad, (unsigned)x->world);
-  k_xunpack<<<grid, 160, 0, c->stream>>>(c->wires, c->Wp, x->d_ids, x->d_offs + level * x->world, x->world, rank,
-                                          pad, d_recv);
+  k_xscatter<<<dim3(1, grid_rows(n)), 160, 0, c->stream>>>(c->wires, c->Wp, x->d_recv_ids + x->recv_off[level], n,
+                                                           d_recv, c->Wp);
   GW_LAUNCHED(c);
   return GW_OK;
+}
+
+int gw_nccl_available(char* why, int64_t why_len) {
+  const NcclApi& api = nccl_api();
+  if (why && why_len > 0) {
+    std::snprintf(why, (size_t)why_len, "%s", api.ok ? "" : api.why.c_str());
+  }
+  if (!api.ok) return 0;
+  int v = 0;
+  api.GetVersion(&v);
+  return v > 0 ? v : 1;
+}
+
+int gw_nccl_unique_id(char* out /* NCCL_UNIQUE_ID_BYTES */) {
+  if (!out) return GW_ERR_ARG;
+  const NcclApi& api = nccl_api();
+  if (!api.ok) return GW_ERR_STATE;
+  ncclUniqueId id;
+  if (api.GetUniqueId(&id) != ncclSuccess) return GW_ERR_CUDA;
+  memcpy(out, id.internal, NCCL_UNIQUE_ID_BYTES);
+  return GW_OK;
+}
+
+int gw_nccl_init(gw_ctx* c, int32_t world, int32_t rank, const char* unique_id) {
+  if (!c || !unique_id || world < 1 || rank < 0 || rank >= world) return GW_ERR_ARG;
+  const NcclApi& api = nccl_api();
+  if (!api.ok) return fail(c, GW_ERR_STATE, "NCCL unavailable: " + api.why);
+  cudaSetDevice(c->device);
+  if (c->nccl) {
+    api.CommDestroy((ncclComm_t)c->nccl);
+    c->nccl = nullptr;
+  }
+  ncclUniqueId id;
+  memcpy(id.internal, unique_id, NCCL_UNIQUE_ID_BYTES);
+  ncclComm_t comm = nullptr;
+  GW_NCCL(c, api, api.CommInitRank(&comm, world, id, rank));
+  c->nccl = comm;
+  c->nccl_world = world;
+  c->nccl_rank = rank;
+  return GW_OK;
+}
+
+int gw_exchange_enqueue(gw_ctx* c, const gw_xplan* x, int64_t level, void* nccl_comm) {
+  if (!c || !x || level < 0 || level >= x->n_levels) return GW_ERR_ARG;
+  ncclComm_t comm = (ncclComm_t)(nccl_comm ? nccl_comm : c->nccl);
+  if (x->world == 1) return GW_OK;
+  if (!comm) return fail(c, GW_ERR_STATE, "no NCCL communicator (gw_nccl_init or pass one)");
+  const NcclApi& api = nccl_api();
+  if (!api.ok) return fail(c, GW_ERR_STATE, "NCCL unavailable: " + api.why);
+  int rc = gw_exchange_pack(c, x, level, nullptr);
+  if (rc) return rc;
+  if (x->send_tot[level] == 0 && x->recv_tot[level] == 0) return GW_OK;
+  cudaSetDevice(c->device);
+  const size_t row_bytes = (size_t)c->Wp * sizeof(uint32_t);
+  // grouped point-to-point: each rank sends only the rows its peers read
+  GW_NCCL(c, api, api.GroupStart());
+  int64_t so = 0, ro = 0;
+  for (int q = 0; q < x->world; ++q) {
+    if (q == x->rank) continue;
+    const int64_t ns = x->send_cnt[level * x->world + q], nr = x->recv_cnt[level * x->world + q];
+    if (ns) {
+      ncclResult_t r = api.Send((const char*)x->d_send + so * row_bytes, (size_t)ns * row_bytes, ncclUint8, q, comm,
+                                c->stream);
+      if (r != ncclSuccess) {
+        api.GroupEnd();
+        return fail(c, GW_ERR_CUDA, std::string("ncclSend: ") + api.GetErrorString(r));
+      }
+    }
+    if (nr) {
+      ncclResult_t r = api.Recv((char*)x->d_recv + ro * row_bytes, (size_t)nr * row_bytes, ncclUint8, q, comm,
+                                c->stream);
+      if (r != ncclSuccess) {
+        api.GroupEnd();
+        return fail(c, GW_ERR_CUDA, std::string("ncclRecv: ") + api.GetErrorString(r));
+      }
+    }
+    so += ns;
+    ro += nr;
+  }
+  GW_NCCL(c, api, api.GroupEnd());
+  return gw_exchange_unpack(c, x, level, nullptr);
 }
 
 int gw_xplan_destroy(gw_ctx* c, gw_xplan* x) {
   if (!x) return GW_OK;
-  if (c) cudaSetDevice(c->device);
-  cudaFree(x->d_offs);
-  cudaFree(x->d_ids);
+  if (c) {
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);  // staging buffers may still be in flight
+  }
+  cudaFree(x->d_send_ids);
+  cudaFree(x->d_recv_ids);
+  cudaFree(x->d_send);
+  cudaFree(x->d_recv);
   delete x;
+  return GW_OK;
+}
+
+// ---- device timeline: event marks on the context stream, read once ----------
+int gw_timeline_reset(gw_ctx* c) {
+  if (!c) return GW_ERR_ARG;
+  for (auto e : c->marks) c->ev_pool.push_back(e);
+  c->marks.clear();
+  return GW_OK;
+}
+
+int gw_timeline_mark(gw_ctx* c) {
+  if (!c) return GW_ERR_ARG;
+  cudaEvent_t e = pooled_event(c);
+  if (!e) return fail(c, GW_ERR_CUDA, "cudaEventCreate failed");
+  GW_CUDA(c, cudaEventRecord(e, c->stream));
+  c->marks.push_back(e);
+  return GW_OK;
+}
+
+int gw_timeline_read(gw_ctx* c, float* ms, int64_t cap, int64_t* count) {
+  if (!c || !count || (cap > 0 && !ms)) return GW_ERR_ARG;
+  const int64_t n = c->marks.empty() ? 0 : (int64_t)c->marks.size() - 1;
+  *count = n;
+  if (n == 0) return GW_OK;
+  GW_CUDA(c, cudaEventSynchronize(c->marks.back()));
+  for (int64_t k = 0; k < n && k < cap; ++k) GW_CUDA(c, cudaEventElapsedTime(&ms[k], c->marks[k], c->marks[k + 1]));
+  return GW_OK;
+}
+
+// All levels [first, last) with one event mark per level boundary and a single
+// host synchronisation at the end; ms[k] = device time of level first + k.
+int gw_plan_run_timed(gw_ctx* c, gw_plan* p, int64_t first, int64_t last, float* ms) {
+  int rc = ready(c);
+  if (rc) return rc;
+  if (!p) return fail(c, GW_ERR_ARG, "null plan");
+  if (first < 0) first = 0;
+  if (last > p->n_levels) last = p->n_levels;
+  if (first >= last) return GW_OK;
+  if (!ms) return GW_ERR_ARG;
+  gw_timeline_reset(c);
+  if ((rc = gw_timeline_mark(c))) return rc;
+  for (int64_t L = first; L < last; ++L) {
+    if ((rc = gw_plan_run_levels(c, p, L, L + 1))) return rc;
+    if ((rc = gw_timeline_mark(c))) return rc;
+  }
+  int64_t n = 0;
+  rc = gw_timeline_read(c, ms, last - first, &n);
+  gw_timeline_reset(c);
+  return rc;
+}
+
+// Rounding-margin probe: blind rotations at N = 1024, l = 2 run the probe build
+// of the kernel, which records max |x - rint(x)| over every value the inverse
+// transforms round (exactness needs < 0.5).
+int gw_set_margin_probe(gw_ctx* c, int on) {
+  if (!c) return GW_ERR_ARG;
+  cudaSetDevice(c->device);
+  GW_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (on && !c->margin) {
+    GW_CUDA(c, cudaMalloc(&c->margin, sizeof(unsigned long long)));
+    GW_CUDA(c, cudaMemset(c->margin, 0, sizeof(unsigned long long)));
+  } else if (!on && c->margin) {
+    cudaFree(c->margin);
+    c->margin = nullptr;
+  }
+  return GW_OK;
+}
+
+int gw_margin_read(gw_ctx* c, double* worst, int reset) {
+  if (!c || !worst) return GW_ERR_ARG;
+  if (!c->margin) return fail(c, GW_ERR_STATE, "margin probe off (gw_set_margin_probe)");
+  cudaSetDevice(c->device);
+  GW_CUDA(c, cudaStreamSynchronize(c->stream));
+  unsigned long long bits = 0;
+  GW_CUDA(c, cudaMemcpy(&bits, c->margin, sizeof(bits), cudaMemcpyDeviceToHost));
+  memcpy(worst, &bits, sizeof(double));
+  if (reset) GW_CUDA(c, cudaMemset(c->margin, 0, sizeof(unsigned long long)));
   return GW_OK;
 }
 

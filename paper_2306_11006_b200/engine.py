@@ -37,8 +37,11 @@ EXPORTS = ("gw_version", "gw_levels", "gw_device_count", "gw_create", "gw_destro
            "gw_eval_gate_batch_device", "gw_wires_alloc", "gw_wires_put", "gw_wires_get",
            "gw_wires_device_ptr", "gw_wires_attach", "gw_plan_create", "gw_plan_run", "gw_plan_run_levels",
            "gw_plan_destroy", "gw_timer_start", "gw_timer_stop", "gw_set_profiling",
-           "gw_stage_times", "gw_br_phase_cycles", "gw_launch_count", "gw_xplan_create", "gw_xplan_pad",
-           "gw_exchange_pack", "gw_exchange_unpack", "gw_xplan_destroy")
+           "gw_stage_times", "gw_br_phase_cycles", "gw_launch_count", "gw_xplan_create",
+           "gw_xplan_peer_rows", "gw_xplan_buffers", "gw_exchange_pack", "gw_exchange_unpack",
+           "gw_exchange_enqueue", "gw_xplan_destroy", "gw_nccl_available", "gw_nccl_unique_id",
+           "gw_nccl_init", "gw_timeline_reset", "gw_timeline_mark", "gw_timeline_read",
+           "gw_plan_run_timed", "gw_set_margin_probe", "gw_margin_read")
 
 
 class EngineUnavailable(RuntimeError):
@@ -101,12 +104,24 @@ def load_library(path: str | None = None):
             "gw_plan_run": ([_P, _P], ctypes.c_int),
             "gw_plan_run_levels": ([_P, _P, ctypes.c_int64, ctypes.c_int64], ctypes.c_int),
             "gw_plan_destroy": ([_P, _P], ctypes.c_int),
-            "gw_xplan_create": ([_P, ctypes.c_int64, ctypes.c_int32, _I64P, _I64P, ctypes.POINTER(_P)],
-                                ctypes.c_int),
-            "gw_xplan_pad": ([_P, _P, ctypes.c_int64, _I64P], ctypes.c_int),
-            "gw_exchange_pack": ([_P, _P, ctypes.c_int64, ctypes.c_int32, _P], ctypes.c_int),
-            "gw_exchange_unpack": ([_P, _P, ctypes.c_int64, ctypes.c_int32, _P], ctypes.c_int),
+            "gw_xplan_create": ([_P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _I64P, _I64P,
+                                 ctypes.POINTER(_P)], ctypes.c_int),
+            "gw_xplan_peer_rows": ([_P, _P, ctypes.c_int64, _I64P, _I64P], ctypes.c_int),
+            "gw_xplan_buffers": ([_P, _P, ctypes.POINTER(_P), ctypes.POINTER(_P)], ctypes.c_int),
+            "gw_exchange_pack": ([_P, _P, ctypes.c_int64, _P], ctypes.c_int),
+            "gw_exchange_unpack": ([_P, _P, ctypes.c_int64, _P], ctypes.c_int),
+            "gw_exchange_enqueue": ([_P, _P, ctypes.c_int64, _P], ctypes.c_int),
             "gw_xplan_destroy": ([_P, _P], ctypes.c_int),
+            "gw_nccl_available": ([ctypes.c_char_p, ctypes.c_int64], ctypes.c_int),
+            "gw_nccl_unique_id": ([ctypes.c_char_p], ctypes.c_int),
+            "gw_nccl_init": ([_P, ctypes.c_int32, ctypes.c_int32, ctypes.c_char_p], ctypes.c_int),
+            "gw_set_margin_probe": ([_P, ctypes.c_int], ctypes.c_int),
+            "gw_margin_read": ([_P, ctypes.POINTER(ctypes.c_double), ctypes.c_int], ctypes.c_int),
+            "gw_timeline_reset": ([_P], ctypes.c_int),
+            "gw_timeline_mark": ([_P], ctypes.c_int),
+            "gw_timeline_read": ([_P, ctypes.POINTER(ctypes.c_float), ctypes.c_int64, _I64P], ctypes.c_int),
+            "gw_plan_run_timed": ([_P, _P, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_float)],
+                                  ctypes.c_int),
             "gw_timer_start": ([_P], ctypes.c_int),
             "gw_timer_stop": ([_P, ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
             "gw_set_profiling": ([_P, ctypes.c_int], ctypes.c_int),
@@ -246,6 +261,36 @@ class Engine:
     def timer_start(self):
         self._check(self._lib.gw_timer_start(self._ctx))
 
+    # rounding-margin probe (exactness evidence)
+    def set_margin_probe(self, on: bool = True):
+        self._check(self._lib.gw_set_margin_probe(self._ctx, 1 if on else 0))
+
+    def margin(self, reset: bool = False) -> float:
+        v = ctypes.c_double(0.0)
+        self._check(self._lib.gw_margin_read(self._ctx, ctypes.byref(v), 1 if reset else 0))
+        return float(v.value)
+
+    # device timeline: marks on the engine stream, one sync when read
+    def timeline_reset(self):
+        self._check(self._lib.gw_timeline_reset(self._ctx))
+
+    def timeline_mark(self):
+        self._check(self._lib.gw_timeline_mark(self._ctx))
+
+    def timeline_read(self) -> list[float]:
+        """Syncs on the last mark; ms between consecutive marks."""
+        n = ctypes.c_int64(0)
+        self._check(self._lib.gw_timeline_read(self._ctx, None, 0, ctypes.byref(n)))
+        buf = (ctypes.c_float * max(1, n.value))()
+        self._check(self._lib.gw_timeline_read(self._ctx, buf, n.value, ctypes.byref(n)))
+        return [float(buf[k]) for k in range(n.value)]
+
+    # native NCCL communicator owned by this context (gw_nccl_init)
+    def nccl_init(self, world: int, rank: int, unique_id: bytes):
+        if len(unique_id) != 128:
+            raise ValueError("an ncclUniqueId is 128 bytes")
+        self._check(self._lib.gw_nccl_init(self._ctx, world, rank, unique_id))
+
     def timer_stop(self) -> float:
         ms = ctypes.c_float(0)
         self._check(self._lib.gw_timer_stop(self._ctx, ctypes.byref(ms)))
@@ -361,20 +406,18 @@ class Engine:
 
 @_serialized
 class ExchangePlanHandle:
-    """Device-resident exchange plan (gw_xplan): pack / unpack one level's wires."""
+    """Device-resident point-to-point exchange plan (gw_xplan): per level, the
+    rows this rank sends to / receives from every peer, with staging buffers."""
 
-    def __init__(self, engine: "Engine", sends, world: int):
-        self.engine, self.world, self.n_levels = engine, world, len(sends)
-        offs, ids = [0], []
-        for lvl in sends:
-            for q in range(world):
-                a = np.asarray(lvl[q], dtype=np.int64)
-                ids.append(a)
-                offs.append(offs[-1] + a.shape[0])
-        self._offs = np.asarray(offs, dtype=np.int64)
-        self._ids = np.concatenate(ids) if ids else np.zeros(0, np.int64)
+    def __init__(self, engine: "Engine", counts, ids, world: int, rank: int):
+        self.engine, self.world, self.rank = engine, world, rank
+        counts = np.ascontiguousarray(counts, dtype=np.int64)
+        self.n_levels = counts.shape[0] if counts.ndim == 3 else 0
+        self._counts = counts.reshape(-1) if counts.size else np.zeros(1, np.int64)
+        self._ids = np.ascontiguousarray(ids, dtype=np.int64) if len(ids) else np.zeros(1, np.int64)
         h = _P()
-        engine._check(engine._lib.gw_xplan_create(engine._ctx, self.n_levels, world, self._offs.ctypes.data_as(_I64P),
+        engine._check(engine._lib.gw_xplan_create(engine._ctx, self.n_levels, world, rank,
+                                                  self._counts.ctypes.data_as(_I64P),
                                                   self._ids.ctypes.data_as(_I64P), ctypes.byref(h)))
         self._h = h
 
@@ -382,21 +425,49 @@ class ExchangePlanHandle:
     def _mtx(self):
         return self.engine._mtx
 
-    def pad(self, level: int) -> int:
-        v = ctypes.c_int64(0)
-        self.engine._check(self.engine._lib.gw_xplan_pad(self.engine._ctx, self._h, level, ctypes.byref(v)))
-        return v.value
+    def peer_rows(self, level: int):
+        s = np.zeros(self.world, np.int64)
+        r = np.zeros(self.world, np.int64)
+        self.engine._check(self.engine._lib.gw_xplan_peer_rows(
+            self.engine._ctx, self._h, level, s.ctypes.data_as(_I64P), r.ctypes.data_as(_I64P)))
+        return s, r
 
-    def pack(self, level: int, rank: int, d_send: int):
-        self.engine._check(self.engine._lib.gw_exchange_pack(self.engine._ctx, self._h, level, rank, _P(d_send)))
+    def buffers(self):
+        ds, dr = _P(), _P()
+        self.engine._check(self.engine._lib.gw_xplan_buffers(self.engine._ctx, self._h, ctypes.byref(ds),
+                                                             ctypes.byref(dr)))
+        return ds.value or 0, dr.value or 0
 
-    def unpack(self, level: int, rank: int, d_recv: int):
-        self.engine._check(self.engine._lib.gw_exchange_unpack(self.engine._ctx, self._h, level, rank, _P(d_recv)))
+    def pack(self, level: int, d_send: int | None = None):
+        self.engine._check(self.engine._lib.gw_exchange_pack(self.engine._ctx, self._h, level, _P(d_send or 0)))
+
+    def unpack(self, level: int, d_recv: int | None = None):
+        self.engine._check(self.engine._lib.gw_exchange_unpack(self.engine._ctx, self._h, level, _P(d_recv or 0)))
+
+    def enqueue(self, level: int, nccl_comm: int | None = None):
+        """pack -> grouped ncclSend/ncclRecv per peer -> unpack, on the engine stream."""
+        self.engine._check(self.engine._lib.gw_exchange_enqueue(self.engine._ctx, self._h, level,
+                                                                _P(nccl_comm or 0)))
 
     def close(self):
         if self._h:
             self.engine._lib.gw_xplan_destroy(self.engine._ctx, self._h)
             self._h = None
+
+
+def nccl_available() -> tuple[int, str]:
+    """(NCCL version code or 0, reason when unavailable)."""
+    why = ctypes.create_string_buffer(256)
+    v = load_library().gw_nccl_available(why, 256)
+    return v, why.value.decode(errors="replace")
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    rc = load_library().gw_nccl_unique_id(buf)
+    if rc != GW_OK:
+        raise RuntimeError(f"ncclGetUniqueId failed ({rc}): {nccl_available()[1]}")
+    return buf.raw
 
 
 @_serialized
@@ -414,6 +485,16 @@ class Plan:
         last = self.n_levels if last is None else last
         e = self.engine
         e._check(e._lib.gw_plan_run_levels(e._ctx, self._h, first, last))
+
+    def run_timed(self, first: int = 0, last: int | None = None) -> list[float]:
+        """All levels back to back, one host sync at the end; device ms per level."""
+        last = self.n_levels if last is None else last
+        if last <= first:
+            return []
+        e = self.engine
+        ms = (ctypes.c_float * (last - first))()
+        e._check(e._lib.gw_plan_run_timed(e._ctx, self._h, first, last, ms))
+        return [float(x) for x in ms]
 
     def close(self):
         if self._h and self._h.value:
@@ -449,11 +530,6 @@ def default_device() -> int:
     return 0
 
 
-_CACHE: "OrderedDict[tuple, tuple]" = OrderedDict()
-_CACHE_MAX = 3
-_cache_lock = threading.Lock()
-
-
 def _host_rows(rows: int, width: int) -> np.ndarray:
     """A fresh (rows, width) u32 array owned by the caller.  When torch is
     importable it is carved from torch's caching pinned-host allocator, so the
@@ -475,33 +551,78 @@ def params_tuple(params):
             int(params.ks_base_bits), int(params.ks_levels), int(params.mu))
 
 
-def engine_for(params, bk_data=None, ksk_data=None, device: int | None = None) -> Engine:
-    """Context with these keys resident, uploaded once and cached.
+# ---------------------------------------------------------------------------
+# Per-key context cache, keyed on the keys' CONTENT.
+#
+# The reference hands the same key arrays to every call (ek.bk.ntt /
+# ek.ksk.data), so a context is cached per (params, device,
+# digest(bk), digest(ksk)).  Hashing 20-80 MB on every 3 ms gate batch would
+# dominate, so a key array is hashed once and then FROZEN (writeable=False): an
+# in-place edit of a key the device already holds raises instead of silently
+# evaluating with the stale upload.  Arrays that cannot be frozen (a view of a
+# writeable buffer) are re-hashed on every call.  Evicted contexts are not
+# closed here: whoever still holds one keeps using it, and it is released when
+# the last reference goes away (Engine.__del__).
+# ---------------------------------------------------------------------------
 
-    The cache key is the identity + data pointer of the key arrays (the
-    reference passes ek.bk.ntt / ek.ksk.data on every call); a
-    strong reference keeps them alive so ids cannot be recycled.
-    """
-    dev = default_device() if device is None else device
-    key = (params_tuple(params), dev,
-           None if bk_data is None else (id(bk_data), bk_data.ctypes.data, bk_data.shape),
-           None if ksk_data is None else (id(ksk_data), ksk_data.ctypes.data, ksk_data.shape))
+_CACHE: "OrderedDict[tuple, Engine]" = OrderedDict()
+_CACHE_MAX = 8
+_cache_lock = threading.Lock()
+_DIGESTS: dict[int, tuple] = {}   # id(array) -> (array, digest); the strong ref pins the id
+
+
+def _frozen(a: np.ndarray) -> bool:
+    x = a
+    while isinstance(x, np.ndarray):
+        if x.flags.writeable:
+            return False
+        x = x.base
+    return True
+
+
+def key_digest(a) -> str:
+    """SHA-256 of a key array's bytes (and shape/dtype), memoised for frozen arrays."""
+    import hashlib
+    hit = _DIGESTS.get(id(a))
+    if hit is not None and hit[0] is a and _frozen(a):
+        return hit[1]
+    arr = np.ascontiguousarray(a)
+    h = hashlib.sha256()
+    h.update(repr((arr.shape, arr.dtype.str)).encode())
+    h.update(memoryview(arr).cast("B"))
+    d = h.hexdigest()
+    try:
+        a.flags.writeable = False
+    except (ValueError, AttributeError):
+        pass
+    if len(_DIGESTS) > 64:
+        _DIGESTS.clear()
+    _DIGESTS[id(a)] = (a, d)
+    return d
+
+
+def engine_for(params, bk_data=None, ksk_data=None, device: int | None = None) -> Engine:
+    """Context with these keys resident, uploaded once and cached by content."""
+    dev = default_device() if device is None else int(device)
     with _cache_lock:
-        hit = _CACHE.get(key)
-        if hit is not None:
+        key = (params_tuple(params), dev,
+               None if bk_data is None else key_digest(bk_data),
+               None if ksk_data is None else key_digest(ksk_data))
+        eng = _CACHE.get(key)
+        if eng is not None and eng.handle.value:
             _CACHE.move_to_end(key)
-            return hit[0]
+            return eng
         eng = Engine(*params_tuple(params), device=dev)
         eng.upload_keys(bk_data, ksk_data)
-        _CACHE[key] = (eng, bk_data, ksk_data)
+        _CACHE[key] = eng
         while len(_CACHE) > _CACHE_MAX:
-            _, (old, _, _) = _CACHE.popitem(last=False)
-            old.close()
+            _CACHE.popitem(last=False)   # not closed: other holders may still use it
         return eng
 
 
 def clear_cache():
     with _cache_lock:
-        for eng, _, _ in _CACHE.values():
+        for eng in _CACHE.values():
             eng.close()
         _CACHE.clear()
+        _DIGESTS.clear()

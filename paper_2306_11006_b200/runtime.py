@@ -8,7 +8,8 @@ and bit-identical outputs for every worker count.  What changed:
   (runtime.py:76-222) become ONE device-resident wire store in HBM and a
   precompiled level plan: per level a single fused launch set (all opcodes of
   the level together) on one CUDA stream, so ordering replaces fences and no
-  host synchronisation happens between levels;
+  host synchronisation happens between levels (one event mark per level
+  boundary, read after the single sync at the end);
 * the SSA guards the reference checks on every read/write (runtime.py:83-96)
   are checked once, statically, over the whole plan before anything runs;
 * with several GPUs (torch.distributed, one process per GPU) each rank runs
@@ -206,14 +207,17 @@ def _cached_plan(c: Circuit, schedule: Schedule, worker: int | None = None,
 
 
 def evaluate(c: Circuit, schedule: Schedule, inputs: Mapping[str, np.ndarray], keys,
-             *, group=None) -> tuple[dict[str, np.ndarray], Metrics]:
+             *, group=None, keep_wires: bool = False) -> tuple[dict[str, np.ndarray], Metrics]:
     """Run every gate of c over encrypted inputs on the GPU(s).
 
     Single process: all of the schedule's worker slices run on this process's
     GPU (the worker split only matters across GPUs).  With a torch.distributed
     process group (`group`, or the default group when initialised and larger
     than one), rank k runs the slices of worker k and levels are joined by the
-    wire exchange; every rank returns the full outputs.
+    wire exchange; every rank returns the full outputs.  keep_wires=True
+    leaves the device wire store allocated (every wire is kept: SSA) so a
+    caller can read intermediate wires back (parity sampling); by default it
+    is released when evaluate returns.
     """
     ek: EvalKey = _as_eval_key(keys)
     p = ek.params
@@ -225,25 +229,35 @@ def evaluate(c: Circuit, schedule: Schedule, inputs: Mapping[str, np.ndarray], k
 
     plan = _cached_plan(c, schedule)
     eng = ek.engine()
-    eng.wires_alloc(c.max_wire + 1)
-    for port in c.inputs:
-        eng.wires_put(np.asarray(port.wires, np.int64), mats[port.name])
     metrics = Metrics(total_gates=len(c.gates), workers=schedule.workers, gpus=1)
-    handle = eng.plan_create(plan.level_offsets, plan.opcodes, plan.operands, plan.out_ids)
-    try:
-        per_wave = []
-        t0 = time.monotonic()
-        for w in range(len(schedule.waves)):
-            s = time.monotonic()
-            eng.timer_start()
-            handle.run(w, w + 1)
-            ms = eng.timer_stop()
-            e = time.monotonic()
-            per_wave.append(ms / 1e3)
-            metrics.spans.append((w, 0, s, e))
-        t1 = time.monotonic()
-    finally:
-        handle.close()
+    # The context is single-submitter: hold it for the whole evaluation so a
+    # concurrent evaluate() on the same keys cannot swap the wire store under
+    # this one (the reference's evaluate is re-entrant, runtime.py:122).
+    with eng._mtx:
+        eng.wires_alloc(c.max_wire + 1)
+        try:
+            for port in c.inputs:
+                eng.wires_put(np.asarray(port.wires, np.int64), mats[port.name])
+            handle = eng.plan_create(plan.level_offsets, plan.opcodes, plan.operands, plan.out_ids)
+            try:
+                # every level enqueued back to back on the engine stream, an event
+                # mark at each level boundary, ONE host synchronisation at the end
+                t0 = time.monotonic()
+                per_wave_ms = handle.run_timed(0, len(schedule.waves))
+                t1 = time.monotonic()
+            finally:
+                handle.close()
+            outputs = {port.name: eng.wires_get(np.asarray(port.wires, np.int64)) for port in c.outputs}
+        except BaseException:
+            eng.wires_alloc(0)
+            raise
+        if not keep_wires:
+            eng.wires_alloc(0)   # release the store (config 4: ~30 GB)
+    per_wave = [ms / 1e3 for ms in per_wave_ms]
+    start = t0
+    for w, dt in enumerate(per_wave):   # spans on the monotonic clock, laid out by device time
+        metrics.spans.append((w, 0, start, start + dt))
+        start += dt
     metrics.bootstrap_count = plan.bootstraps
     metrics.ntt_forward_count = 2 * p.l * p.n * plan.bootstraps
     metrics.ntt_inverse_count = 2 * p.n * plan.bootstraps
@@ -253,7 +267,6 @@ def evaluate(c: Circuit, schedule: Schedule, inputs: Mapping[str, np.ndarray], k
                                 if metrics.wall_time_seconds > 0 else 0.0)
     metrics.per_wave_wall_time = per_wave
     metrics.per_worker_busy_time = [metrics.device_time_seconds] + [0.0] * (schedule.workers - 1)
-    outputs = {port.name: eng.wires_get(np.asarray(port.wires, np.int64)) for port in c.outputs}
     return outputs, metrics
 
 

@@ -99,7 +99,8 @@ def test_evaluate_errors(mini_keys):
 
 
 def test_exchange_pack_unpack_kernels(p128_keys):
-    """gw_exchange_pack / _unpack move exactly the planned wire rows."""
+    """gw_exchange_pack / _unpack move exactly the planned wire rows, grouped by
+    destination (pack) and by source (unpack)."""
     import torch
     from paper_2306_11006_b200.cggi import PARAM_128
     from paper_2306_11006_b200.engine import Engine, ExchangePlanHandle, params_tuple
@@ -108,24 +109,37 @@ def test_exchange_pack_unpack_kernels(p128_keys):
     eng.wires_alloc(slots)
     rows = np.random.default_rng(5).integers(0, 2 ** 32, (slots, W), dtype=np.uint32)
     eng.wires_put(np.arange(slots), rows)
-    sends = [[np.array([3, 7, 9]), np.array([20, 21])], [np.array([], np.int64), np.array([40])]]
-    x = ExchangePlanHandle(eng, sends, 2)
-    assert [x.pad(0), x.pad(1)] == [3, 1]
+    # 3 ranks, 2 levels; this is rank 0.  counts[L][src][dst]
+    counts = np.zeros((2, 3, 3), np.int64)
+    cells = {(0, 0, 1): [3, 7], (0, 0, 2): [9], (0, 1, 0): [20, 21], (0, 2, 0): [30],
+             (0, 1, 2): [22], (1, 2, 0): [40]}
+    ids = []
+    for L in range(2):
+        for q in range(3):
+            for r in range(3):
+                cell = cells.get((L, q, r), [])
+                counts[L, q, r] = len(cell)
+                ids += cell
+    x = ExchangePlanHandle(eng, counts, np.array(ids, np.int64), 3, 0)
+    sr, rr = x.peer_rows(0)
+    assert sr.tolist() == [0, 2, 1] and rr.tolist() == [0, 2, 1]
     stride = eng.row_stride
     send = torch.zeros((3, stride), dtype=torch.int32, device="cuda")
-    x.pack(0, 0, send.data_ptr())
+    x.pack(0, send.data_ptr())
     torch.cuda.synchronize()
     assert np.array_equal(send[:, :W].cpu().numpy().view(np.uint32), rows[[3, 7, 9]])
-    # rank 0 receives rank 1's rows of level 0 (wires 20, 21) from a fabricated all-gather
-    recv = torch.zeros((2 * 3, stride), dtype=torch.int32, device="cuda")
-    new = np.random.default_rng(6).integers(0, 2 ** 32, (2, W), dtype=np.uint32)
-    recv[3:5, :W] = torch.from_numpy(new.view(np.int32)).cuda()
-    x.unpack(0, 0, recv.data_ptr())
+    recv = torch.zeros((3, stride), dtype=torch.int32, device="cuda")
+    new = np.random.default_rng(6).integers(0, 2 ** 32, (3, W), dtype=np.uint32)
+    recv[:, :W] = torch.from_numpy(new.view(np.int32)).cuda()
+    x.unpack(0, recv.data_ptr())        # rank 1's wires 20, 21 then rank 2's wire 30
     torch.cuda.synchronize()
     got = eng.wires_get(np.arange(slots))
     want = rows.copy()
-    want[[20, 21]] = new
+    want[[20, 21, 30]] = new
     assert np.array_equal(got, want)
+    # plan-owned staging buffers
+    ds, dr = x.buffers()
+    assert ds and dr
     x.close()
 
 

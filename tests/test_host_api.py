@@ -138,7 +138,33 @@ def test_engine_methods_are_serialised():
     from paper_2306_11006_b200 import engine as E
     for cls, names in ((E.Engine, ("eval_gate_batch", "blind_rotate", "keyswitch", "wires_put",
                                    "wires_get", "plan_create", "sync", "upload_keys")),
-                       (E.Plan, ("run", "close")),
-                       (E.ExchangePlanHandle, ("pack", "unpack", "pad", "close"))):
+                       (E.Plan, ("run", "run_timed", "close")),
+                       (E.ExchangePlanHandle, ("pack", "unpack", "peer_rows", "enqueue", "close"))):
         for n in names:
             assert hasattr(getattr(cls, n), "__wrapped__"), f"{cls.__name__}.{n} is not serialised"
+
+
+def test_api_golden_inputs_reproduced(mini_keys, p128_keys):
+    """keygen + encrypt_bits reproduce the operands the reference encrypted
+    for tests/golden/api.npz (so the GPU wrappers see identical bytes)."""
+    import os
+    from conftest import GOLDEN, MINI
+    from paper_2306_11006_b200.cggi import PARAM_128, encrypt_bits
+    from paper_2306_11006_b200.rng import SeededRng
+    g = dict(np.load(os.path.join(GOLDEN, "api.npz")))
+    for tag, ks, p, seed in (("mini", mini_keys, MINI, 2024), ("p128", p128_keys, PARAM_128, 7)):
+        bits = np.random.default_rng(500 + seed).integers(0, 2, g[f"{tag}_bits"].shape)
+        assert np.array_equal(bits, g[f"{tag}_bits"])
+        rng = SeededRng(500 + seed)
+        for k in range(3):
+            assert np.array_equal(encrypt_bits(p, ks.lwe_sk, bits[k], rng), g[f"{tag}_ct{k}"])
+
+
+def test_sample_extract_matches_reference_golden():
+    import os
+    from conftest import GOLDEN
+    from paper_2306_11006_b200.cggi import TlweCiphertext, sample_extract
+    g = dict(np.load(os.path.join(GOLDEN, "api.npz")))
+    for tag in ("mini", "p128"):
+        got = np.stack([sample_extract(TlweCiphertext(a)).vec for a in g[f"{tag}_blind_rotate"]])
+        assert np.array_equal(got, g[f"{tag}_sample_extract"])
