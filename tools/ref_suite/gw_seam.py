@@ -15,6 +15,10 @@ Every call is counted; a call the engine cannot take (unknown key array) falls
 back to the reference kernel and is reported, so the summary shows how much of
 the suite actually ran through the GPU.  Test infrastructure only.
 
+Seam 3 (GW_SEAM=3, with tests/test_cli.py) swaps the reference's CLI `main`
+for paper_2306_11006_b200.cli.main (keygen / encrypt / run on the GPU /
+decrypt / analyze / gen, same arguments, outputs and exit codes).
+
 Usage (tools/ref_suite/run.sh): PYTHONPATH=baseline/_ref:tools/ref_suite:. \
     python -m pytest baseline/_ref/_tests -p gw_seam
 """
@@ -87,6 +91,18 @@ def pytest_configure(config):
 
         ref.eval_gate_batch = eval_gate_batch
         rt.eval_gate_batch = eval_gate_batch
+    if os.environ.get("GW_SEAM", "1") == "3":
+        # Seam 3: the reference's CLI tests (tests/test_cli.py binds `main` at
+        # import, after this hook) drive OUR command line, whose `run` evaluates
+        # on the B200 through paper_2306_11006_b200.runtime.evaluate.
+        import gatewave.cli as rcli
+        from paper_2306_11006_b200 import cli as mycli
+
+        def main(argv=None):
+            STATS["cli_gpu"] += 1
+            return mycli.main(argv)
+
+        rcli.main = main
 
 
 def pytest_terminal_summary(terminalreporter, exitstatus, config):
