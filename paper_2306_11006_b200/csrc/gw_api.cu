@@ -24,6 +24,7 @@
 #include "blind_rotate.cuh"
 #include "br_tmem.cuh"
 #include "br_v3.cuh"
+#include "br_v3w.cuh"
 #include "gates.cuh"
 #include "keyswitch.cuh"
 #include "ks_tc.cuh"
@@ -96,6 +97,8 @@ struct gw_ctx {
   int br_variant = 2;
   int br_gc = 0;  // v3 gates per CTA override (GATEWAVE_BR_GC, measurement only; 0 = by batch size)
   bool br_gc1_tma = false;
+  int br_w = 0;        // gate-interleaved v3w kernel: gates per warp (GATEWAVE_BR_W=GW,GC; 0 = policy)
+  int br_wgc = 1;
   bool br_ldr = true;  // loader warps at GC = 2, 3 (GATEWAVE_BR_LDR=0: LDG by the compute warps)  // GATEWAVE_BR_GC1=tma: one-gate CTAs stage the key through shared memory
   std::vector<cudaEvent_t> marks;  // device timeline (gw_timeline_*)
   void* nccl = nullptr;            // ncclComm_t owned by the context (gw_nccl_init)
@@ -310,6 +313,30 @@ int launch_v3_g(gw_ctx* c, const BrArgs& a0) {
   return GW_OK;
 }
 
+template <int GW, int GC, bool PROBE = false>
+int launch_v3w_g(gw_ctx* c, const BrArgs& a0) {
+  BrArgs a = a0;
+  a.bk = c->bk_v3;
+  a.margin = PROBE ? c->margin : nullptr;
+  const size_t smem = V3W::smem_bytes(GW * GC);
+  if (int rc = set_smem(c, k_blind_rotate_v3w<GW, GC, PROBE>, smem)) return rc;
+  a.gates_per_cta = GW * GC;
+  const int grid = (a.B + GW * GC - 1) / (GW * GC);
+  k_blind_rotate_v3w<GW, GC, PROBE><<<grid, 128 * GC + 128, smem, c->stream>>>(a);
+  GW_LAUNCHED(c);
+  return GW_OK;
+}
+
+int launch_v3w(gw_ctx* c, const BrArgs& a, int gw, int gc) {
+  if (c->margin) {
+    if (gw == 2 && gc == 2) return launch_v3w_g<2, 2, true>(c, a);
+    return launch_v3w_g<2, 1, true>(c, a);
+  }
+  if (gw == 2 && gc == 2) return launch_v3w_g<2, 2>(c, a);
+  if (gw == 3) return launch_v3w_g<3, 1>(c, a);
+  return launch_v3w_g<2, 1>(c, a);
+}
+
 // v3: one CTA per SM holding GC gates.  GC minimises waves x step time, with the
 // measured per-step cycles of each configuration (profiles/r01_v3_gc_sweep.txt):
 // GC=1 7.8k (loader warps), GC=2 9.6k, GC=3 12.6k (loader warps + setmaxnreg + stagger),
@@ -327,6 +354,7 @@ int launch_v3(gw_ctx* c, const BrArgs& a) {
     }
   }
   if (c->br_gc > 0) gc = c->br_gc;
+  if (c->br_w >= 2) return launch_v3w(c, a, c->br_w, c->br_wgc);
   if (c->margin) {  // rounding-margin probe build: loader-warp variants only
     if (gc >= 3) return launch_v3_g<3, 2, true>(c, a);
     if (gc == 2) return launch_v3_g<2, 2, true>(c, a);
@@ -730,6 +758,11 @@ int gw_create(int device, gw_ctx** out) {
   if (const char* v = getenv("GATEWAVE_BR_GC")) c->br_gc = atoi(v);
   if (const char* v = getenv("GATEWAVE_BR_GC1")) c->br_gc1_tma = strcmp(v, "tma") == 0;
   if (const char* v = getenv("GATEWAVE_BR_LDR")) c->br_ldr = atoi(v) != 0;
+  if (const char* v = getenv("GATEWAVE_BR_W")) {  // "GW,GC": force the gate-interleaved kernel (measurement)
+    c->br_w = atoi(v);
+    const char* comma = strchr(v, ',');
+    c->br_wgc = comma ? atoi(comma + 1) : 1;
+  }
   if (const char* v = getenv("GATEWAVE_BR_KERNEL"))
     c->br_variant = strcmp(v, "v1") == 0 ? 0 : strcmp(v, "v2") == 0 ? 1 : 2;
   if (const char* v = getenv("GATEWAVE_KS_KERNEL")) c->ks_variant = strcmp(v, "cuda") == 0 ? 0 : 1;
