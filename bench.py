@@ -546,7 +546,13 @@ def run_ours(args):
         which = ([] if ws == 1 else ["config4"] + (["config5"] if ws == 8 else [])) \
             if args.sharded == "auto" else [x for x in args.sharded.split(",") if x]
         if which:
-            sharded = {name: netlist_sharded(name, ks, P, dist, rank, ws) for name in which}
+            sharded = {}
+            for name in which:
+                # a failure here must not cost the config-1 line: report it instead
+                try:
+                    sharded[name] = netlist_sharded(name, ks, P, dist, rank, ws)
+                except Exception as e:  # noqa: BLE001
+                    sharded[name] = {"error": f"{type(e).__name__}: {e}"[:500]}
 
     # ---- CPU baseline: the unmodified reference, rank 0 at N=1 only ---------
     cpu = cpu_c2 = cpu_c345 = None

@@ -31,6 +31,12 @@ struct BrArgs {
   // rounding-margin probe (gw_set_margin_probe): max |x - rint(x)| over every
   // FP64 value the inverse transforms round, as the bits of a positive double
   unsigned long long* margin = nullptr;
+  // fused gate prologue (v3): when jobs != nullptr, gate g's LWE row is
+  // w0*rows[src0] + w1*rows[src1] (+ cmu*mu on the body) instead of lin[g]
+  const LinJob* jobs = nullptr;
+  const uint32_t* rows = nullptr;
+  int64_t row_stride = 0;
+  uint32_t mu = 0;
 };
 
 // Bootstrapping key, FFT domain: [i][c][h][s][r][lane] complex, scaled by 1/M.

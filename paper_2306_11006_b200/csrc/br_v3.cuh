@@ -125,6 +125,7 @@ __device__ __forceinline__ void tm_cp_128x256b(uint32_t taddr, uint64_t desc) {
   asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(desc) : "memory");
 }
 
+
 // Key streaming modes (KM).  2, the default for GC <= 3: four loader warps
 // (one per TMEM sub-partition) load each slab with 16-24 coalesced 16-byte
 // loads in flight and store it with tcgen05.st, up to two steps ahead (chunks
@@ -180,7 +181,24 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
   const bool active = g < a.B;
   // inactive gate slots (last CTA) run on row 0 and discard the result, so the
   // barrier protocol never depends on the batch size
-  const uint32_t* lin_g = a.lin + (size_t)(active ? g : 0) * a.lin_stride;
+  const uint32_t* lin_g = a.jobs ? nullptr : a.lin + (size_t)(active ? g : 0) * a.lin_stride;
+  // fused gate prologue: the LWE row of a bootstrap is the gate's
+  // linear combination of its operand rows, read straight from the wire store
+  const uint32_t* src0 = nullptr;
+  const uint32_t* src1 = nullptr;
+  uint32_t w0 = 1, w1 = 0, body_add = 0;
+  if (a.jobs) {
+    const LinJob jb = a.jobs[active ? g : 0];
+    src0 = a.rows + (size_t)jb.src[0] * a.row_stride;
+    src1 = jb.src[1] >= 0 ? a.rows + (size_t)jb.src[1] * a.row_stride : src0;
+    w0 = (uint32_t)jb.w[0];
+    w1 = jb.src[1] >= 0 ? (uint32_t)jb.w[1] : 0u;
+    body_add = (uint32_t)jb.cmu * a.mu;
+  }
+  auto lin_at = [&](int k) -> uint32_t {
+    if (!a.jobs) return __ldg(lin_g + k);
+    return w0 * __ldg(src0 + k) + w1 * __ldg(src1 + k) + (k == a.n ? body_add : 0u);
+  };
 
   if (threadIdx.x == 0) {
     for (int k = 0; k < 2; ++k) {
@@ -297,9 +315,10 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
 
   uint32_t* acc_g = acc_all + (size_t)gl * 2 * N;
   double2* U = ubuf_all + (size_t)gl * UB;
+
   // acc <- tv * X^{-bbar} (cggi.py:612-622): warp o < 2 initialises component o
   if (warp < 4 * GC && o < 2) {
-    const uint32_t bbar = ((lin_g[a.n] + radd) >> rshift) & two_n_mask;
+    const uint32_t bbar = ((lin_at(a.n) + radd) >> rshift) & two_n_mask;
     const uint32_t k = (2 * N - bbar) & two_n_mask;
     const uint32_t* tvc = a.tv + o * N;
     for (int j = lane; j < N; j += 32) {
@@ -384,7 +403,7 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
   // 0's F(0) (GW_STAGGER2).
   constexpr bool kStagger = LDR && (GC == 3 || GC == 2);
   if (kStagger && gl >= 1) mbar_wait(&go_bar[gl - 1], 0);
-  uint32_t a_next = __ldg(lin_g);
+  uint32_t a_next = lin_at(0);
   uint32_t sink = 0;  // GW_ABL & 8 only
   double worst = 0.0;  // PROBE only
   for (int i = 0; i < a.n; ++i) {
@@ -393,7 +412,7 @@ __global__ void __launch_bounds__(128 * GC + (KM == 2 ? 128 : 0), 1) k_blind_rot
     const bool pre = i + 1 < a.n;
     const uint32_t a_i = a_next;
     if (pre) {
-      a_next = __ldg(lin_g + i + 1);
+      a_next = lin_at(i + 1);
       kissue(i + 1, 0);
     }
     // ---------------- F: row r = o ----------------

@@ -19,12 +19,6 @@ __host__ __device__ inline unsigned grid_rows(int64_t rows) {
   return (unsigned)(rows < 1 ? 1 : rows > 65535 ? 65535 : rows);
 }
 
-struct LinJob {        // lin = w0*row(s0) + w1*row(s1) + cmu*mu on the body word
-  int32_t src[2];
-  int32_t w[2];
-  int32_t cmu;
-  int32_t pad;
-};
 
 struct CheapUnit {     // bootstrap-free gate
   int32_t kind;        // 0 COPY, 1 NOT, 2 CONST0, 3 CONST1

@@ -24,7 +24,6 @@
 #include "blind_rotate.cuh"
 #include "br_tmem.cuh"
 #include "br_v3.cuh"
-#include "br_v3w.cuh"
 #include "gates.cuh"
 #include "keyswitch.cuh"
 #include "ks_tc.cuh"
@@ -97,9 +96,8 @@ struct gw_ctx {
   int br_variant = 2;
   int br_gc = 0;  // v3 gates per CTA override (GATEWAVE_BR_GC, measurement only; 0 = by batch size)
   bool br_gc1_tma = false;
-  int br_w = 0;        // gate-interleaved v3w kernel: gates per warp (GATEWAVE_BR_W=GW,GC; 0 = policy)
-  int br_wgc = 1;
-  bool br_ldr = true;  // loader warps at GC = 2, 3 (GATEWAVE_BR_LDR=0: LDG by the compute warps)  // GATEWAVE_BR_GC1=tma: one-gate CTAs stage the key through shared memory
+  bool br_ldr = true;
+  bool br_unfused = false;  // GATEWAVE_BR_UNFUSED=1: separate k_lin launch (A/B)  // loader warps at GC = 2, 3 (GATEWAVE_BR_LDR=0: LDG by the compute warps)  // GATEWAVE_BR_GC1=tma: one-gate CTAs stage the key through shared memory
   std::vector<cudaEvent_t> marks;  // device timeline (gw_timeline_*)
   void* nccl = nullptr;            // ncclComm_t owned by the context (gw_nccl_init)
   unsigned long long* margin = nullptr;  // rounding-margin probe accumulator (gw_set_margin_probe)
@@ -313,30 +311,6 @@ int launch_v3_g(gw_ctx* c, const BrArgs& a0) {
   return GW_OK;
 }
 
-template <int GW, int GC, bool PROBE = false>
-int launch_v3w_g(gw_ctx* c, const BrArgs& a0) {
-  BrArgs a = a0;
-  a.bk = c->bk_v3;
-  a.margin = PROBE ? c->margin : nullptr;
-  const size_t smem = V3W::smem_bytes(GW * GC);
-  if (int rc = set_smem(c, k_blind_rotate_v3w<GW, GC, PROBE>, smem)) return rc;
-  a.gates_per_cta = GW * GC;
-  const int grid = (a.B + GW * GC - 1) / (GW * GC);
-  k_blind_rotate_v3w<GW, GC, PROBE><<<grid, 128 * GC + 128, smem, c->stream>>>(a);
-  GW_LAUNCHED(c);
-  return GW_OK;
-}
-
-int launch_v3w(gw_ctx* c, const BrArgs& a, int gw, int gc) {
-  if (c->margin) {
-    if (gw == 2 && gc == 2) return launch_v3w_g<2, 2, true>(c, a);
-    return launch_v3w_g<2, 1, true>(c, a);
-  }
-  if (gw == 2 && gc == 2) return launch_v3w_g<2, 2>(c, a);
-  if (gw == 3) return launch_v3w_g<3, 1>(c, a);
-  return launch_v3w_g<2, 1>(c, a);
-}
-
 // v3: one CTA per SM holding GC gates.  GC minimises waves x step time, with the
 // measured per-step cycles of each configuration (profiles/r01_v3_gc_sweep.txt):
 // GC=1 7.8k (loader warps), GC=2 9.6k, GC=3 12.6k (loader warps + setmaxnreg + stagger),
@@ -354,7 +328,6 @@ int launch_v3(gw_ctx* c, const BrArgs& a) {
     }
   }
   if (c->br_gc > 0) gc = c->br_gc;
-  if (c->br_w >= 2) return launch_v3w(c, a, c->br_w, c->br_wgc);
   if (c->margin) {  // rounding-margin probe build: loader-warp variants only
     if (gc >= 3) return launch_v3_g<3, 2, true>(c, a);
     if (gc == 2) return launch_v3_g<2, 2, true>(c, a);
@@ -554,10 +527,21 @@ int run_level(gw_ctx* c, const uint32_t* src, int64_t src_stride, uint32_t* dst,
               const LinJob* jobs, int J, const KsUnit* units, int U, const CheapUnit* cheap, int C) {
   int rc;
   if (J > 0) {
-    if ((rc = ensure(c, &c->lin, &c->lin_cap, (size_t)J * c->Wp, sizeof(uint32_t)))) return rc;
+    // v3 computes each bootstrap's linear combination in its prologue (fused
+    // k_lin); the other kernels read materialised rows
+    const bool fused = c->logn == 10 && c->p.l == 2 && c->br_variant == 2 && c->bk_v3 && !c->br_unfused;
     if ((rc = ensure(c, &c->acc, &c->acc_cap, (size_t)J * 2 * c->p.N, sizeof(uint32_t)))) return rc;
-    if ((rc = staged(c, 2, 0, [&] { return launch_lin(c, src, src_stride, jobs, J); }))) return rc;
+    if (!fused) {
+      if ((rc = ensure(c, &c->lin, &c->lin_cap, (size_t)J * c->Wp, sizeof(uint32_t)))) return rc;
+      if ((rc = staged(c, 2, 0, [&] { return launch_lin(c, src, src_stride, jobs, J); }))) return rc;
+    }
     BrArgs a;
+    if (fused) {
+      a.jobs = jobs;
+      a.rows = src;
+      a.row_stride = src_stride;
+      a.mu = c->p.mu;
+    }
     a.lin = c->lin;
     a.lin_stride = c->Wp;
     a.B = J;
@@ -758,11 +742,8 @@ int gw_create(int device, gw_ctx** out) {
   if (const char* v = getenv("GATEWAVE_BR_GC")) c->br_gc = atoi(v);
   if (const char* v = getenv("GATEWAVE_BR_GC1")) c->br_gc1_tma = strcmp(v, "tma") == 0;
   if (const char* v = getenv("GATEWAVE_BR_LDR")) c->br_ldr = atoi(v) != 0;
-  if (const char* v = getenv("GATEWAVE_BR_W")) {  // "GW,GC": force the gate-interleaved kernel (measurement)
-    c->br_w = atoi(v);
-    const char* comma = strchr(v, ',');
-    c->br_wgc = comma ? atoi(comma + 1) : 1;
-  }
+  if (const char* v = getenv("GATEWAVE_BR_UNFUSED")) c->br_unfused = atoi(v) != 0;
+
   if (const char* v = getenv("GATEWAVE_BR_KERNEL"))
     c->br_variant = strcmp(v, "v1") == 0 ? 0 : strcmp(v, "v2") == 0 ? 1 : 2;
   if (const char* v = getenv("GATEWAVE_KS_KERNEL")) c->ks_variant = strcmp(v, "cuda") == 0 ? 0 : 1;

@@ -13,6 +13,16 @@
 
 namespace gw {
 
+// A bootstrap's input: lin = w0*row(s0) + w1*row(s1) + cmu*mu on the body word
+// (cggi.py:816-830, the per-kind combination).  k_lin materialises it; the v3
+// blind rotation computes it on the fly from the operand rows.
+struct LinJob {
+  int32_t src[2];
+  int32_t w[2];
+  int32_t cmu;
+  int32_t pad;
+};
+
 // e^{2 pi i t / 64}, t in [0, 64): every root of unity the in-register DFTs
 // use (sizes divide 64).  Filled from the host with correctly rounded values.
 __constant__ double2 c_root64[64];
