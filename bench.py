@@ -442,10 +442,10 @@ def run_ours(args):
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     step_kcyc = {1: 7.8, 2: 9.6, 3: 12.6, 4: 17.7}   # gw_api.cu launch_v3 policy
     gc = min(step_kcyc, key=lambda g: (-(-G // (sms * g)) * step_kcyc[g], g))
-    kname = f"k_blind_rotate_v3<{gc},{0 if gc == 4 else 2}>"
+    kname = f"k_blind_rotate_v3<{gc}, {0 if gc == 4 else 2}, false>"
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")) as f:
             t = json.load(f).get(kname)
         if t and t["gates"] == G:
             traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
@@ -453,7 +453,7 @@ def run_ours(args):
         pass
     roofline = {"bound": "fp64", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-                "traffic_unit": "bytes per launch (ncu dram read+write, profiles/r01_ncu_traffic.json)",
+                "traffic_unit": "bytes per launch (ncu dram read+write, profiles/r02_ncu_traffic.json)",
                 "kernel": kname,
                 "per_launch_ms": br_ms / launches_br,
                 "work_per_launch": f"{G} bootstraps x {flops_per_bootstrap} FLOP",

@@ -139,7 +139,9 @@ def main():
             "netlist": name, "gates": len(c.gates), "bootstraps": nb, "levels": len(sched.waves),
             "max_level_gates": max(sum(len(b.gate_ids) for b in w) for w in sched.waves),
             "app_latency_s": app, "app_latency_first_s": lat[0], "gates_per_s": len(c.gates) / app, "bootstraps_per_s": nb / app,
-            "device_time_s": met.device_time_seconds, "decrypt_ok": bool(ok),
+            "device_time_s": met.device_time_seconds, "metrics_wall_time_s": met.wall_time_seconds,
+            "wall_over_device": met.wall_time_seconds / met.device_time_seconds if met.device_time_seconds else None,
+            "decrypt_ok": bool(ok),
             "input_bits": int(sum(p.width for p in c.inputs)), "output_bits": int(sum(p.width for p in c.outputs)),
             "host_prep": prep, **({"per_vector": per_vec} if per_vec else {})})
     if rank == 0:
