@@ -95,9 +95,9 @@ struct gw_ctx {
   // 1: v2 TMEM 4-warp kernel, 0: v1 2-warp kernel (GATEWAVE_BR_KERNEL=v3|v2|v1)
   int br_variant = 2;
   int br_gc = 0;  // v3 gates per CTA override (GATEWAVE_BR_GC, measurement only; 0 = by batch size)
-  bool br_gc1_tma = false;
-  bool br_ldr = true;
-  bool br_unfused = false;  // GATEWAVE_BR_UNFUSED=1: separate k_lin launch (A/B)  // loader warps at GC = 2, 3 (GATEWAVE_BR_LDR=0: LDG by the compute warps)  // GATEWAVE_BR_GC1=tma: one-gate CTAs stage the key through shared memory
+  bool br_gc1_tma = false;  // GATEWAVE_BR_GC1=tma: one-gate CTAs stage the key through shared memory
+  bool br_ldr = true;       // loader warps at GC = 2, 3 (GATEWAVE_BR_LDR=0: LDG by the compute warps)
+  bool br_unfused = false;  // GATEWAVE_BR_UNFUSED=1: separate k_lin launch (A/B)
   std::vector<cudaEvent_t> marks;  // device timeline (gw_timeline_*)
   void* nccl = nullptr;            // ncclComm_t owned by the context (gw_nccl_init)
   unsigned long long* margin = nullptr;  // rounding-margin probe accumulator (gw_set_margin_probe)
@@ -920,6 +920,7 @@ int gw_upload_keys(gw_ctx* c, const uint32_t* bk_coeff, const uint32_t* ksk) {
       }
       if (e != cudaSuccess) rc = fail(c, GW_ERR_CUDA, std::string("v3 key image: ") + cudaGetErrorString(e));
     }
+
     cudaError_t es = cudaStreamSynchronize(c->stream);
     cudaFree(bk_dev);
     if (rc) return rc;
