@@ -921,6 +921,7 @@ int gw_upload_keys(gw_ctx* c, const uint32_t* bk_coeff, const uint32_t* ksk) {
       if (e != cudaSuccess) rc = fail(c, GW_ERR_CUDA, std::string("v3 key image: ") + cudaGetErrorString(e));
     }
 
+
     cudaError_t es = cudaStreamSynchronize(c->stream);
     cudaFree(bk_dev);
     if (rc) return rc;
