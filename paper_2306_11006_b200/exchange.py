@@ -13,6 +13,7 @@ Levels stay stream-ordered: run level -> pack -> ncclSend/ncclRecv per peer
 """
 from __future__ import annotations
 
+import contextlib
 import time
 from dataclasses import dataclass
 
@@ -212,6 +213,9 @@ def evaluate_distributed(c: Circuit, schedule: Schedule, mats: dict, ek: EvalKey
     if dx is not None and dist.get_backend(group) == "nccl":
         native = _native_comm(lv.eng, group, world, rank)
     stride = wires.shape[1]
+    # single-submitter context: hold it for the whole evaluation (as runtime.evaluate does)
+    lock = lv.eng._mtx if hasattr(lv, "eng") else contextlib.nullcontext()
+    lock.__enter__()
     try:
         for port in c.inputs:
             ids = torch.as_tensor(np.asarray(port.wires, np.int64), device=device)
@@ -269,7 +273,10 @@ def evaluate_distributed(c: Circuit, schedule: Schedule, mats: dict, ek: EvalKey
             ids = torch.as_tensor(np.asarray(port.wires, np.int64), device=device)
             outputs[port.name] = wires[ids, :W].cpu().numpy().view(np.uint32).copy()
     finally:
-        lv.close()
+        try:
+            lv.close()
+        finally:
+            lock.__exit__(None, None, None)
     # whole-job metrics: wall time is the max over ranks
     cdev = device if dist.get_backend(group) == "nccl" else torch.device("cpu")
     t = torch.tensor([t1 - t0] + per_wave, dtype=torch.float64, device=cdev)
