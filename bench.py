@@ -71,6 +71,10 @@ def _args():
                     help="netlists evaluated sharded over the GPUs: auto (config4 at N>1, + config5 at "
                          "N=8), none, or a comma list of config4,config5,config3")
     ap.add_argument("--no-cpu-netlists", action="store_true")
+    # test-only: exercise the N > 1 flow on a single-GPU box (every rank on GPU 0, gloo
+    # process group, host-staged wire exchange) -- NCCL cannot put two ranks on one GPU
+    ap.add_argument("--backend", choices=("nccl", "gloo"), default="nccl", help=argparse.SUPPRESS)
+    ap.add_argument("--same-device", action="store_true", help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -348,10 +352,15 @@ def config2_latency(ks, P, eng, repeats: int = 3):
 def run_ours(args):
     import torch
     ws, rank, local = _dist()
+    if args.same_device:
+        local = 0
     if ws > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     else:
         dist = None
         torch.cuda.set_device(local)
@@ -365,7 +374,7 @@ def run_ours(args):
     def max_over_ranks(x: float) -> float:
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if args.backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -642,7 +651,7 @@ def netlist_sharded(name, ks, P, dist, rank, ws):
     torch.cuda.synchronize()
     app = time.monotonic() - t0
     if dist is not None:
-        tl = torch.tensor([app], dtype=torch.float64, device="cuda")
+        tl = torch.tensor([app], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(tl, op=dist.ReduceOp.MAX)
         app = float(tl.item())
     h = hashlib.sha256()

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import contextlib
 import time
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -138,7 +139,7 @@ class _DeviceLevels:
         self.eng.wires_alloc(0)
 
 
-_NCCL_COMMS: dict = {}
+_NCCL_COMMS: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()  # engine -> (group, world)
 
 
 def _native_comm(eng, group, world: int, rank: int) -> bool:
@@ -146,15 +147,15 @@ def _native_comm(eng, group, world: int, rank: int) -> bool:
     and group): rank 0's ncclUniqueId travels over the process group."""
     import torch.distributed as dist
     from .engine import nccl_available, nccl_unique_id
-    key = (id(eng), id(group) if group is not None else None, world)
-    if _NCCL_COMMS.get(key) is eng:
+    key = (id(group) if group is not None else None, world)
+    if _NCCL_COMMS.get(eng) == key:
         return True
     if not nccl_available()[0]:
         return False
     obj = [nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
     eng.nccl_init(world, rank, obj[0])
-    _NCCL_COMMS[key] = eng
+    _NCCL_COMMS[eng] = key
     return True
 
 
