@@ -107,10 +107,9 @@ def exchange_plan(c: Circuit, schedule: Schedule, world: int) -> ExchangePlan:
 class _DeviceLevels:
     """Adapter: the CUDA engine running one rank's level plan on a torch wire store."""
 
-    def __init__(self, ek: EvalKey, plan, slots: int, device):
+    def __init__(self, eng, plan, slots: int, device):
         import torch
-        # the engine must live on the same GPU as the wire tensor (ADVICE r1)
-        self.eng = ek.engine(device=device.index)
+        self.eng = eng
         self.stream = torch.cuda.current_stream(device)
         if self.stream.cuda_stream == 0:
             self.stream = torch.cuda.Stream(device)
@@ -200,24 +199,31 @@ def evaluate_distributed(c: Circuit, schedule: Schedule, mats: dict, ek: EvalKey
     plan = _cached_plan(c, schedule, worker=rank, world=world)
     xp = exchange_plan(c, schedule, world)
     slots = c.max_wire + 1
+    # the engine lives on the same GPU as the wire tensor, and the context is
+    # single-submitter: it is held for the whole evaluation (as runtime.evaluate does)
+    lock = contextlib.nullcontext()
     if levels_factory is None:
         device = torch.device("cuda", torch.cuda.current_device())
-        lv = _DeviceLevels(ek, plan, slots, device)
+        eng = ek.engine(device=device.index)
+        lock = eng._mtx
+        lock.__enter__()
+        try:
+            lv = _DeviceLevels(eng, plan, slots, device)
+        except BaseException:
+            lock.__exit__(None, None, None)
+            raise
     else:
         device = torch.device("cpu")
         lv = levels_factory(plan, slots, device)
     wires = lv.wires
     W = p.n + 1
     levels = len(schedule.waves)
-    dx = lv.exchange_plan(xp, rank) if hasattr(lv, "exchange_plan") else None
-    native = False
-    if dx is not None and dist.get_backend(group) == "nccl":
-        native = _native_comm(lv.eng, group, world, rank)
     stride = wires.shape[1]
-    # single-submitter context: hold it for the whole evaluation (as runtime.evaluate does)
-    lock = lv.eng._mtx if hasattr(lv, "eng") else contextlib.nullcontext()
-    lock.__enter__()
+    dx, native = None, False
     try:
+        dx = lv.exchange_plan(xp, rank) if hasattr(lv, "exchange_plan") else None
+        if dx is not None and dist.get_backend(group) == "nccl":
+            native = _native_comm(lv.eng, group, world, rank)
         for port in c.inputs:
             ids = torch.as_tensor(np.asarray(port.wires, np.int64), device=device)
             wires[ids, :W] = torch.from_numpy(mats[port.name].view(np.int32)).to(device)
