@@ -183,6 +183,14 @@ int gw_br_phase_cycles(gw_ctx* ctx, long long* out);
  * recovered the exact integer). */
 int gw_set_margin_probe(gw_ctx* ctx, int on);
 int gw_margin_read(gw_ctx* ctx, double* worst, int reset);
+/* Exact mode.  Off (default): at N = 1024, l = 2 with every
+ * convolution coefficient <= 2^51 (PARAM_128, PARAM_110) the blind rotation
+ * uses ONE FFT image of the 32-bit key words (v5: half the inverse transforms
+ * and MACs of the split key; exactness measured by the margin probe, not
+ * proven).  On: the split-key kernel (v3), whose FP64 exactness is proven.
+ * Also GATEWAVE_BR_EXACT=1 at context creation. */
+int gw_set_exact(gw_ctx* ctx, int on);
+int gw_get_exact(gw_ctx* ctx, int* on);
 /* Number of engine kernel launches issued by this context so far. */
 int gw_launch_count(gw_ctx* ctx, int64_t* count);
 

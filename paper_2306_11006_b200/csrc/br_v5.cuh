@@ -1,0 +1,407 @@
+// br_v5.cuh -- blind rotation v5: the v3 structure (frequency-partitioned MAC,
+// key streamed L2 -> loader warps -> TMEM ring, lane twiddles in TMEM) with the
+// bootstrapping key held as ONE FFT image of its full 32-bit words instead of
+// two 16-bit halves.  Reference: gatewave/cggi.py:592-667 (`_blind_rotate_kernel`),
+// PARAM_128 / PARAM_110 geometry (N = 1024, l = 2: four gadget rows).
+//
+// Per step and gate the external product is 4 forward FFT-512 (one per gadget
+// row, as in v3), 8 complex MACs per frequency (v3: 16) and 2 inverse FFT-512
+// (one per accumulator component; v3: 4, one per component and key half).
+// The key slab of a step is 64 KB (v3: 128 KB) and the HBM image 41 MB, the
+// size of the reference's own NTT-domain key (cggi.py:283-285).
+//
+// Exactness: every coefficient the inverse transforms round is an
+// integer of magnitude <= 2l N 2^(Bg-1) 2^31 = 2^51 at PARAM_128 / PARAM_110.
+// The FP64 error of the transform chain is no longer provably below 1/2 at
+// that magnitude; it is MEASURED (probe build, tests/test_gpu_margin.py):
+// every rounded value lies within a few hundredths of an integer, so the
+// outputs are bit-identical to the exact (split-key, v3) path and to the
+// reference on every tested input.  The worst-case analytic bound still
+// limits any deviation to a few units of 2^-32 per coefficient and step,
+// far inside the decryption margin (the north star's "stated noise bound").
+// GATEWAVE_BR_EXACT=1 (gw_set_exact) selects the split-key v3 kernel.
+//
+// CTA = GC gates x 4 compute warps + 4 key-loader warps, one CTA per SM.
+//   F  warp r: rotate-subtract, gadget digits, fold + twist, forward head of row r
+//   M  warp w: frequency pairs (k1, c), c in [4w, 4w+4): last forward radix-2
+//      stage of the 4 rows, 2 outputs x 4 rows complex MACs against the key
+//      values in TMEM, first inverse radix-2 stage -> V rows 0, 1
+//   I  two of the four warps (alternating by step and gate, so the four SMSPs
+//      share the inverse work): inverse tail of component o, untwist, round,
+//      acc[o] += v (one writer per word).
+// TMEM (512 columns): 3 key slabs of 128 columns (slab i in slot i mod 3) +
+// the lane twiddle table (64 columns).  The loader warps run up to two steps
+// ahead of the MAC: slab i waits for MAC(i - 3) to release its slot.
+#pragma once
+#include "br_v3.cuh"
+
+namespace gw {
+
+struct V5 {
+  static constexpr int LOGN = 10, LEV = 2;
+  using G = Geo<LOGN>;
+  static constexpr int N = G::N, M = G::M, P = G::P, L = G::L, R = 2 * LEV;
+  static constexpr int CIDX = 32;                   // key complexes per TMEM lane per step: 4 freqs x (2 outputs x 4 rows)
+  static constexpr int COLS = CIDX * 4;             // TMEM columns per slab (128)
+  static constexpr int NSLOT = 3;                   // slabs resident in TMEM
+  static constexpr int TWCOL = NSLOT * COLS;        // lane twiddles: columns 384..447
+  static constexpr int UB = R * P * L;              // double2 per gate: U / V / transpose tiles (32 KB)
+  static constexpr int XCHG = 2 * 2 * (P / 2) * 32; // u32 per gate: digit swap between level-warps
+  static constexpr int SLAB = CIDX * 128 * 16;      // key bytes per step (64 KB)
+  static size_t smem_bytes(int gc) {
+    return (size_t)gc * (UB * sizeof(double2) + 2 * N * sizeof(uint32_t) + XCHG * sizeof(uint32_t)) + 256;
+  }
+};
+
+// key image: [i][cidx][tmem lane] complex, cidx = q*8 + o*4 + r (q = 2p + s as in v3,
+// o = accumulator component, r = gadget row), tmem lane = 32*w + lane.
+__host__ __device__ __forceinline__ size_t v5_index(int i, int cidx, int tlane) {
+  return ((size_t)i * V5::CIDX + cidx) * 128 + tlane;
+}
+
+#ifndef GW_V5_LREG2
+#define GW_V5_LREG2 64
+#endif
+#ifndef GW_V5_LREG3
+#define GW_V5_LREG3 56
+#endif
+
+template <int GC, bool PROBE = false>
+__global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a) {
+  static_assert(GC >= 1 && GC <= 3, "loader warps need registers the compute warps can spare");
+  constexpr int LREG = GC == 1 ? 0 : GC == 2 ? GW_V5_LREG2 : GW_V5_LREG3;
+  constexpr int kPool = ((65536 / (128 * GC + 128)) & ~7) * (128 * GC + 128);
+  constexpr int CREG = GC == 1 ? 0 : ((kPool - LREG * 128) / (128 * GC)) & ~7;
+  using G = V5::G;
+  constexpr int N = V5::N, M = V5::M, P = V5::P, L = V5::L, R = V5::R, LEV = V5::LEV, LOGN = V5::LOGN;
+  constexpr int UB = V5::UB, COLS = V5::COLS, CIDX = V5::CIDX, NSLOT = V5::NSLOT;
+
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  double2* ubuf_all = reinterpret_cast<double2*>(smem_raw);  // GC x [row][c][pos]
+  uint32_t* acc_all = reinterpret_cast<uint32_t*>(ubuf_all + (size_t)GC * UB);
+  uint32_t* xchg_all = acc_all + (size_t)GC * 2 * N;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xchg_all + (size_t)GC * V5::XCHG);
+  uint64_t* full_bar = bars;           // [3] the loader warps stored slab i in slot i % 3
+  uint64_t* empty_bar = bars + NSLOT;  // [3] every compute warp finished its MAC reads of slot i % 3
+  uint64_t* go_bar = bars + 2 * NSLOT; // [2] stagger: gate 0 reached its start points for gates 1 / 2
+  uint32_t* tm_slot = reinterpret_cast<uint32_t*>(bars + 2 * NSLOT + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, l = lane;
+  const int gl = warp >> 2, o = warp & 3;
+  const int g = blockIdx.x * GC + gl;
+  const bool active = g < a.B;
+  // inactive gate slots (last CTA) run on row 0 and discard the result
+  const uint32_t* lin_g = a.jobs ? nullptr : a.lin + (size_t)(active ? g : 0) * a.lin_stride;
+  const uint32_t* src0 = nullptr;
+  const uint32_t* src1 = nullptr;
+  uint32_t w0 = 1, w1 = 0, body_add = 0;
+  if (a.jobs) {  // fused gate prologue, as in v3
+    const LinJob jb = a.jobs[active ? g : 0];
+    src0 = a.rows + (size_t)jb.src[0] * a.row_stride;
+    src1 = jb.src[1] >= 0 ? a.rows + (size_t)jb.src[1] * a.row_stride : src0;
+    w0 = (uint32_t)jb.w[0];
+    w1 = jb.src[1] >= 0 ? (uint32_t)jb.w[1] : 0u;
+    body_add = (uint32_t)jb.cmu * a.mu;
+  }
+  auto lin_at = [&](int k) -> uint32_t {
+    if (!a.jobs) return __ldg(lin_g + k);
+    return w0 * __ldg(src0 + k) + w1 * __ldg(src1 + k) + (k == a.n ? body_add : 0u);
+  };
+
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < NSLOT; ++k) {
+      mbar_init(&full_bar[k], 4);
+      mbar_init(&empty_bar[k], 4 * GC);
+    }
+    mbar_init(&go_bar[0], 4);
+    mbar_init(&go_bar[1], 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tm_alloc(tm_slot, 512);
+  tm_fence_before();
+  __syncthreads();
+  tm_fence_after();
+  const uint32_t tm_base = *tm_slot;
+  const uint32_t tm_warp = tm_base + ((uint32_t)(32 * o) << 16);
+  const uint32_t tm_tw = tm_warp + (uint32_t)V5::TWCOL;
+  if (gl == 0 && warp < 4 * GC) {
+#pragma unroll
+    for (int k1 = 0; k1 < P; ++k1) tm_st4(tm_tw + (uint32_t)(4 * k1), __ldg(a.tables + 2 * G::TILE + k1 * L + l));
+    tm_wait_st();
+  }
+
+  const uint32_t two_n_mask = 2 * N - 1;
+  const uint32_t rshift = 32 - (LOGN + 1);
+  const uint32_t radd = 1u << (32 - (LOGN + 1) - 1);
+  const uint32_t base_mask = (1u << a.bg_bits) - 1;
+  const int32_t half_base = 1 << (a.bg_bits - 1);
+  const double dmagic = 6755399441055744.0 + (double)half_base;
+
+  uint32_t* acc_g = acc_all + (size_t)gl * 2 * N;
+  double2* U = ubuf_all + (size_t)gl * UB;
+
+  // acc <- tv * X^{-bbar} (cggi.py:612-622): warp o < 2 initialises component o
+  if (warp < 4 * GC && o < 2) {
+    const uint32_t bbar = ((lin_at(a.n) + radd) >> rshift) & two_n_mask;
+    const uint32_t k = (2 * N - bbar) & two_n_mask;
+    const uint32_t* tvc = a.tv + o * N;
+    for (int j = lane; j < N; j += 32) {
+      const uint32_t m = ((uint32_t)j - k) & two_n_mask;
+      acc_g[o * N + j] = m < (uint32_t)N ? tvc[m] : 0u - tvc[m - N];
+    }
+  }
+  tm_fence_before();
+  __syncthreads();
+  tm_fence_after();
+
+  const int mk1 = lane & 15;
+  const int mc0 = 4 * o + 2 * (lane >> 4);
+  const int pos = v3_pos(l);
+  const int bar_id = 1 + gl;
+
+  const bool prof = a.prof != nullptr && blockIdx.x == 0 && gl == 0 && lane == 0;
+  long long pt_[6] = {0, 0, 0, 0, 0, 0};
+  long long tprev = clock64();
+  auto mark = [&](int ph) {
+    if (prof) {
+      const long long t = clock64();
+      pt_[ph] += t - tprev;
+      tprev = t;
+    }
+  };
+
+  if (warp >= 4 * GC) {
+    // ---- loader warp: slab i -> TMEM slot i % 3 of sub-partition o ----
+    if constexpr (GC >= 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(LREG));
+    const double2* src_w = a.bk + (size_t)32 * o + lane;
+    int slot = 0;
+    for (int i = 0; i < a.n; ++i) {
+      const double2* src = src_w + (size_t)i * CIDX * 128;
+#if GW_L2PF
+      if (o == 0 && lane == 0 && i + GW_L2PF < a.n) {
+        const char* pf = reinterpret_cast<const char*>(a.bk + (size_t)(i + GW_L2PF) * CIDX * 128);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf), "r"(V5::SLAB) : "memory");
+      }
+#endif
+      if (i >= NSLOT) {
+        mbar_wait(&empty_bar[slot], (uint32_t)(((i - NSLOT) / NSLOT) & 1));
+        tm_fence_after();
+      }
+      const uint32_t dst = tm_warp + (uint32_t)(slot * COLS);
+#pragma unroll 1
+      for (int rnd = 0; rnd < CIDX / 16; ++rnd) {
+        double2 v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = ldg_stream(src + (size_t)(rnd * 16 + k) * 128);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) tm_st4(dst + (uint32_t)((rnd * 16 + k) * 4), v[k]);
+      }
+      tm_wait_st();
+      tm_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full_bar[slot]);
+      slot = slot + 1 == NSLOT ? 0 : slot + 1;
+    }
+  } else {
+    if constexpr (GC >= 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(CREG));
+    // stagger (as v3): gate 1 starts after gate 0's F(0), gate 2 after its M(0)
+    constexpr bool kStagger = GC >= 2;
+    if (kStagger && gl >= 1) mbar_wait(&go_bar[gl - 1], 0);
+    uint32_t a_next = lin_at(0);
+    double worst = 0.0;  // PROBE only
+    int slot = 0;
+    for (int i = 0; i < a.n; ++i) {
+      const uint32_t a_i = a_next;
+      if (i + 1 < a.n) a_next = lin_at(i + 1);
+      // ---------------- F: row r = o (identical to v3) ----------------
+      {
+        const int cr = o / LEV, lv = o % LEV;
+        const uint32_t* A = acc_g + cr * N;
+        const uint32_t abar = ((a_i + radd) >> rshift) & two_n_mask;
+        const uint32_t idx0 = ((uint32_t)l - abar) & two_n_mask;
+        double2 x[P];
+        const int hh = lv;
+        const int sh_mine = 32 - (lv + 1) * a.bg_bits, sh_other = 32 - (2 - lv) * a.bg_bits;
+        uint32_t* xg = xchg_all + (size_t)gl * V5::XCHG + (size_t)cr * 2 * (P / 2) * 32;
+        uint32_t* to_partner = xg + (size_t)(1 - lv) * (P / 2) * 32;
+        const uint32_t* from_partner = xg + (size_t)lv * (P / 2) * 32;
+        uint32_t mine[P];
+        const uint32_t idxh = idx0 + (uint32_t)(hh * M);
+#pragma unroll
+        for (int m1 = 0; m1 < P; m1 += 2) {
+          uint32_t oth[2];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const uint32_t idx = (idxh + (uint32_t)(L * (m1 + q))) & two_n_mask;
+            const uint32_t v = A[idx & (N - 1)];
+            const uint32_t neg = 0u - ((idx >> LOGN) & 1u);
+            const uint32_t buf = ((v ^ neg) - neg) - A[L * (m1 + q) + l + hh * M] + a.offs;
+            mine[m1 + q] = (buf >> sh_mine) & base_mask;
+            oth[q] = (buf >> sh_other) & base_mask;
+          }
+          to_partner[(m1 / 2) * 32 + lane] = oth[0] | (oth[1] << 16);
+        }
+        named_barrier(5 + 2 * gl + cr, 64);
+#pragma unroll
+        for (int m1 = 0; m1 < P; m1 += 2) {
+          const uint32_t w = from_partner[(m1 / 2) * 32 + lane];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const uint32_t rv = q ? (w >> 16) : (w & 0xFFFFu);
+            const uint32_t re = hh ? rv : mine[m1 + q], im = hh ? mine[m1 + q] : rv;
+            double2 v = make_double2(digit_to_double_lo(re, dmagic), digit_to_double_lo(im, dmagic));
+            if (m1 + q > 0) v = cmul(v, c_root64[G::CSTEP * (m1 + q)]);
+            x[bitrev_c<G::LOGP>(m1 + q)] = v;
+          }
+        }
+        double2* tile = U + (size_t)o * P * L;
+        fft_forward_head<LOGN, true>(x, tile, TwTmemHalves{tm_tw}, l);
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < P; ++c) tile[c * L + pos] = x[c];
+      }
+      if (kStagger && i == 0 && gl == 0 && lane == 0) mbar_arrive(&go_bar[0]);
+      mark(0);
+      named_barrier(bar_id, 128);  // U complete
+      mark(1);
+      // ---------------- M: frequency pairs (mk1, mc0 + p), 2 outputs x 4 rows ----------------
+      mbar_wait(&full_bar[slot], (uint32_t)((i / NSLOT) & 1));
+      tm_fence_after();
+      const uint32_t tm_slab = tm_warp + (uint32_t)(slot * COLS);
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const int c = mc0 + p;
+        const double2 tw = c_root64[2 * c];  // e^{2 pi i c / 32}
+        uint32_t kw[2][32];
+        // both s halves of this pair's keys: 2 x 32 columns (8 complex each)
+#pragma unroll
+        for (int s = 0; s < 2; ++s) tm_ld_raw<32>(tm_slab + (uint32_t)((2 * p + s) * 32), kw[s]);
+        double2 D[R][2];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const double2* row = U + ((size_t)r * P + c) * L;
+          const double2 u0 = row[v3_slot(mk1, 0)], u1 = row[v3_slot(mk1, 1)];
+          const double2 t = cmul(u1, tw);
+          D[r][0] = cadd(u0, t);
+          D[r][1] = csub(u0, t);
+        }
+        tm_wait_ld();
+        double2 O[2][2];  // [output][s]
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+#pragma unroll
+          for (int oo = 0; oo < 2; ++oo)
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              const uint32_t* k4 = kw[s] + (oo * 4 + r) * 4;
+              const double2 kr = make_double2(__hiloint2double(k4[1], k4[0]), __hiloint2double(k4[3], k4[2]));
+              O[oo][s] = r == 0 ? cmul(D[r][s], kr) : cfma(O[oo][s], D[r][s], kr);
+            }
+#pragma unroll
+        for (int oo = 0; oo < 2; ++oo) {
+          double2* row = U + ((size_t)oo * P + c) * L;
+          row[v3_slot(mk1, 0)] = cadd(O[oo][0], O[oo][1]);
+          row[v3_slot(mk1, 1)] = cmulc(csub(O[oo][0], O[oo][1]), tw);
+        }
+      }
+      tm_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[slot]);
+      if (kStagger && i == 0 && gl == 0 && lane == 0) mbar_arrive(&go_bar[1]);
+      mark(2);
+      named_barrier(bar_id, 128);  // V complete
+      mark(3);
+      // ---------------- I: output oo = component oo, two warps per gate ----------------
+      const int isel = (i + gl) & 1;  // which warp pair inverts this step
+      if ((o >> 1) == isel) {
+        const int oo = o & 1;
+        double2 x[P];
+        double2* tile = U + (size_t)oo * P * L;
+#pragma unroll
+        for (int c = 0; c < P; ++c) x[bitrev_c<G::LOGP>(c)] = tile[c * L + pos];
+        fft_inverse_tail<LOGN, true>(x, tile, TwTmemHalves{tm_tw}, l);
+        if (active) {
+          uint32_t* Ac = acc_g + oo * N;
+#pragma unroll
+          for (int m1 = 0; m1 < P; ++m1) {
+            const double2 v = m1 == 0 ? x[0] : cmulc(x[m1], c_root64[G::CSTEP * m1]);
+            const uint32_t j = (uint32_t)(L * m1 + l);
+            if constexpr (PROBE) worst = fmax(worst, fmax(fabs(v.x - rint(v.x)), fabs(v.y - rint(v.y))));
+            Ac[j] += round_mod32(v.x);
+            Ac[j + M] += round_mod32(v.y);
+          }
+        }
+      }
+      mark(4);
+      named_barrier(bar_id, 128);  // acc updated before the next decomposition
+      mark(5);
+      slot = slot + 1 == NSLOT ? 0 : slot + 1;
+    }
+    if constexpr (PROBE) {
+#pragma unroll
+      for (int d = 16; d >= 1; d >>= 1) worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, d));
+      if (lane == 0 && active && a.margin) atomicMax(a.margin, (unsigned long long)__double_as_longlong(worst));
+    }
+    if (prof)
+      for (int ph = 0; ph < 6; ++ph) a.prof[o * 6 + ph] = pt_[ph];
+    if (active && o < 2) {
+      uint32_t* dst = a.acc_out + ((size_t)g * 2 + o) * N;
+      for (int j = lane; j < N; j += 32) dst[j] = acc_g[o * N + j];
+    }
+  }
+  tm_fence_before();
+  __syncthreads();
+  if (warp == 0) tm_dealloc(tm_base, 512);
+}
+
+// Key image for v5 (reference: cggi.py:283-285 keeps the NTT-domain copy).  One
+// warp per (i, r, c) polynomial: the full signed 32-bit words, fold + twist, the
+// forward head, the last radix-2 stage for every (k1, c) pair, scaled by 1/M and
+// scattered to [i][cidx][tmem lane].
+__global__ void __launch_bounds__(128) k_bk_to_v5(const uint32_t* __restrict__ bk_coeff, int n,
+                                                  const double2* __restrict__ tables, double2* __restrict__ img) {
+  using G = V5::G;
+  constexpr int N = V5::N, M = V5::M, P = V5::P, L = V5::L, R = V5::R;
+  __shared__ double2 tw1[P * L];
+  __shared__ double2 tiles[4][P * L];
+  for (int t = threadIdx.x; t < P * L; t += blockDim.x) tw1[t] = tables[2 * G::TILE + t];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, l = lane;
+  const long long job = (long long)blockIdx.x * 4 + warp;  // (i*R + r)*2 + c
+  if (job >= (long long)n * R * 2) return;
+  const int c = (int)(job & 1);
+  const int r = (int)((job >> 1) % R);
+  const int i = (int)((job >> 1) / R);
+  const uint32_t* poly = bk_coeff + (((size_t)i * R + r) * 2 + c) * N;
+  double2 x[P];
+#pragma unroll
+  for (int m1 = 0; m1 < P; ++m1) {
+    double2 v = make_double2((double)(int32_t)poly[L * m1 + l], (double)(int32_t)poly[L * m1 + l + M]);
+    if (m1 > 0) v = cmul(v, c_root64[G::CSTEP * m1]);
+    x[bitrev_c<G::LOGP>(m1)] = v;
+  }
+  double2* tile = tiles[warp];
+  fft_forward_head<V5::LOGN, true>(x, tile, TwSmem{tw1, L, l}, l);
+  __syncwarp();
+#pragma unroll
+  for (int cc = 0; cc < P; ++cc) tile[cc * L + v3_pos(l)] = x[cc];
+  __syncwarp();
+  const double scale = 1.0 / (double)M;
+  const int k1 = lane & 15;
+#pragma unroll
+  for (int w = 0; w < 4; ++w)
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const int cf = 4 * w + 2 * (lane >> 4) + p;
+      const double2 u0 = tile[cf * L + v3_slot(k1, 0)], u1 = tile[cf * L + v3_slot(k1, 1)];
+      const double2 t = cmul(u1, c_root64[2 * cf]);
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const double2 d = s ? csub(u0, t) : cadd(u0, t);
+        const int cidx = (2 * p + s) * 8 + c * 4 + r;
+        img[v5_index(i, cidx, 32 * w + lane)] = make_double2(d.x * scale, d.y * scale);
+      }
+    }
+}
+
+}  // namespace gw

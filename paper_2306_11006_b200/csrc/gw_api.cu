@@ -24,6 +24,7 @@
 #include "blind_rotate.cuh"
 #include "br_tmem.cuh"
 #include "br_v3.cuh"
+#include "br_v5.cuh"
 #include "gates.cuh"
 #include "keyswitch.cuh"
 #include "ks_tc.cuh"
@@ -55,6 +56,7 @@ struct gw_ctx {
   double2* bk_fft = nullptr;
   size_t bk_fft_count = 0;
   double2* bk_v3 = nullptr;    // v3 key image (br_v3.cuh), N = 1024 and l = 2 only
+  double2* bk_v5 = nullptr;    // v5 single key image (br_v5.cuh), where v5 applies (v5_ok)
   uint32_t* ksk = nullptr;
   uint8_t* kimg = nullptr;     // keyswitch key as INT8 tensor-core B image (ks_tc.cuh)
   int kt_ntiles = 0, kt_kblocks = 0;
@@ -98,6 +100,7 @@ struct gw_ctx {
   bool br_gc1_tma = false;  // GATEWAVE_BR_GC1=tma: one-gate CTAs stage the key through shared memory
   bool br_ldr = true;       // loader warps at GC = 2, 3 (GATEWAVE_BR_LDR=0: LDG by the compute warps)
   bool br_unfused = false;  // GATEWAVE_BR_UNFUSED=1: separate k_lin launch (A/B)
+  bool br_exact = false;    // gw_set_exact / GATEWAVE_BR_EXACT=1: split-key v3 kernel instead of v5
   std::vector<cudaEvent_t> marks;  // device timeline (gw_timeline_*)
   void* nccl = nullptr;            // ncclComm_t owned by the context (gw_nccl_init)
   unsigned long long* margin = nullptr;  // rounding-margin probe accumulator (gw_set_margin_probe)
@@ -339,8 +342,54 @@ int launch_v3(gw_ctx* c, const BrArgs& a) {
   return c->br_gc1_tma ? launch_v3_g<1, 1>(c, a) : launch_v3_g<1, 2>(c, a);
 }
 
+template <int GC, bool PROBE = false>
+int launch_v5_g(gw_ctx* c, const BrArgs& a0) {
+  BrArgs a = a0;
+  a.bk = c->bk_v5;
+  a.margin = PROBE ? c->margin : nullptr;
+  const size_t smem = V5::smem_bytes(GC);
+  if (int rc = set_smem(c, k_blind_rotate_v5<GC, PROBE>, smem)) return rc;
+  a.gates_per_cta = GC;
+  const int grid = (a.B + GC - 1) / GC;
+  k_blind_rotate_v5<GC, PROBE><<<grid, 128 * GC + 128, smem, c->stream>>>(a);
+  GW_LAUNCHED(c);
+  return GW_OK;
+}
+
+// v5 (single key image): GC minimises waves x step time over the measured
+// per-step cycles of each configuration.
+int launch_v5(gw_ctx* c, const BrArgs& a) {
+  static const double kStep[4] = {0, 6.5, 8.19, 10.63};  // k cycles per step, profiles/r02_v5_first.txt
+  int gc = 1;
+  double best = 1e300;
+  for (int g = 1; g <= 3; ++g) {
+    const double waves = (double)((a.B + (int64_t)c->sm_count * g - 1) / ((int64_t)c->sm_count * g));
+    const double t = waves * kStep[g];
+    if (t < best * 0.999) {
+      best = t;
+      gc = g;
+    }
+  }
+  if (c->br_gc > 0) gc = c->br_gc > 3 ? 3 : c->br_gc;
+  if (c->margin) {
+    if (gc == 3) return launch_v5_g<3, true>(c, a);
+    if (gc == 2) return launch_v5_g<2, true>(c, a);
+    return launch_v5_g<1, true>(c, a);
+  }
+  if (gc == 3) return launch_v5_g<3>(c, a);
+  if (gc == 2) return launch_v5_g<2>(c, a);
+  return launch_v5_g<1>(c, a);
+}
+
+// v5 applies at N = 1024, l = 2 when every convolution coefficient with the
+// full 32-bit key word stays within 2^51 (the round_mod32 range): PARAM_128 / PARAM_110.
+bool v5_ok(const gw_ctx* c) {
+  return c->logn == 10 && c->p.l == 2 && std::log2(2.0 * c->p.l) + c->logn + (c->p.bg_bits - 1) + 31 <= 51.0 + 1e-9;
+}
+
 template <int LOGN>
 int launch_br_n(gw_ctx* c, const BrArgs& a) {
+  if (LOGN == 10 && c->p.l == 2 && c->br_variant == 2 && !c->br_exact && c->bk_v5) return launch_v5(c, a);
   if (LOGN == 10 && c->p.l == 2 && c->br_variant == 2 && c->bk_v3) return launch_v3(c, a);
   switch (c->p.l) {
     case 1: return c->br_variant ? launch_tm<LOGN, 1>(c, a) : launch_br_t<LOGN, 1>(c, a);
@@ -743,6 +792,7 @@ int gw_create(int device, gw_ctx** out) {
   if (const char* v = getenv("GATEWAVE_BR_GC1")) c->br_gc1_tma = strcmp(v, "tma") == 0;
   if (const char* v = getenv("GATEWAVE_BR_LDR")) c->br_ldr = atoi(v) != 0;
   if (const char* v = getenv("GATEWAVE_BR_UNFUSED")) c->br_unfused = atoi(v) != 0;
+  if (const char* v = getenv("GATEWAVE_BR_EXACT")) c->br_exact = atoi(v) != 0;
 
   if (const char* v = getenv("GATEWAVE_BR_KERNEL"))
     c->br_variant = strcmp(v, "v1") == 0 ? 0 : strcmp(v, "v2") == 0 ? 1 : 2;
@@ -765,6 +815,7 @@ int gw_destroy(gw_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   cudaFree(c->bk_fft);
   cudaFree(c->bk_v3);
+  cudaFree(c->bk_v5);
   cudaFree(c->ksk);
   cudaFree(c->kimg);
   cudaFree(c->ks_ut);
@@ -919,6 +970,19 @@ int gw_upload_keys(gw_ctx* c, const uint32_t* bk_coeff, const uint32_t* ksk) {
         if (e == cudaSuccess) c->launches++;
       }
       if (e != cudaSuccess) rc = fail(c, GW_ERR_CUDA, std::string("v3 key image: ") + cudaGetErrorString(e));
+    }
+    cudaFree(c->bk_v5);
+    c->bk_v5 = nullptr;
+    if (rc == GW_OK && v5_ok(c)) {
+      const size_t cnt = (size_t)n * V5::CIDX * 128;
+      e = cudaMalloc(&c->bk_v5, cnt * sizeof(double2));
+      if (e == cudaSuccess) {
+        const long long jobs = (long long)n * 2 * l * 2;
+        k_bk_to_v5<<<(unsigned)((jobs + 3) / 4), 128, 0, c->stream>>>(bk_dev, n, c->tables, c->bk_v5);
+        e = cudaGetLastError();
+        if (e == cudaSuccess) c->launches++;
+      }
+      if (e != cudaSuccess) rc = fail(c, GW_ERR_CUDA, std::string("v5 key image: ") + cudaGetErrorString(e));
     }
 
 
@@ -1646,6 +1710,20 @@ int gw_set_margin_probe(gw_ctx* c, int on) {
     cudaFree(c->margin);
     c->margin = nullptr;
   }
+  return GW_OK;
+}
+
+// Exact mode: the split-key v3 blind rotation (provable FP64 exactness) instead
+// of v5 (single key image, measured exactness); DESIGN.md §3.
+int gw_set_exact(gw_ctx* c, int on) {
+  if (!c) return GW_ERR_ARG;
+  c->br_exact = on != 0;
+  return GW_OK;
+}
+
+int gw_get_exact(gw_ctx* c, int* on) {
+  if (!c || !on) return GW_ERR_ARG;
+  *on = c->br_exact ? 1 : 0;
   return GW_OK;
 }
 

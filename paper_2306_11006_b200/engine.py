@@ -41,7 +41,7 @@ EXPORTS = ("gw_version", "gw_levels", "gw_device_count", "gw_create", "gw_destro
            "gw_xplan_peer_rows", "gw_xplan_buffers", "gw_exchange_pack", "gw_exchange_unpack",
            "gw_exchange_enqueue", "gw_xplan_destroy", "gw_nccl_available", "gw_nccl_unique_id",
            "gw_nccl_init", "gw_timeline_reset", "gw_timeline_mark", "gw_timeline_read",
-           "gw_plan_run_timed", "gw_set_margin_probe", "gw_margin_read")
+           "gw_plan_run_timed", "gw_set_margin_probe", "gw_margin_read", "gw_set_exact", "gw_get_exact")
 
 
 class EngineUnavailable(RuntimeError):
@@ -116,6 +116,8 @@ def load_library(path: str | None = None):
             "gw_nccl_unique_id": ([ctypes.c_char_p], ctypes.c_int),
             "gw_nccl_init": ([_P, ctypes.c_int32, ctypes.c_int32, ctypes.c_char_p], ctypes.c_int),
             "gw_set_margin_probe": ([_P, ctypes.c_int], ctypes.c_int),
+            "gw_set_exact": ([_P, ctypes.c_int], ctypes.c_int),
+            "gw_get_exact": ([_P, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
             "gw_margin_read": ([_P, ctypes.POINTER(ctypes.c_double), ctypes.c_int], ctypes.c_int),
             "gw_timeline_reset": ([_P], ctypes.c_int),
             "gw_timeline_mark": ([_P], ctypes.c_int),
@@ -264,6 +266,15 @@ class Engine:
     # rounding-margin probe (exactness evidence)
     def set_margin_probe(self, on: bool = True):
         self._check(self._lib.gw_set_margin_probe(self._ctx, 1 if on else 0))
+
+    # exact mode: split-key v3 blind rotation instead of the single-image v5
+    def set_exact(self, on: bool = True):
+        self._check(self._lib.gw_set_exact(self._ctx, 1 if on else 0))
+
+    def exact(self) -> bool:
+        v = ctypes.c_int(0)
+        self._check(self._lib.gw_get_exact(self._ctx, ctypes.byref(v)))
+        return bool(v.value)
 
     def margin(self, reset: bool = False) -> float:
         v = ctypes.c_double(0.0)
