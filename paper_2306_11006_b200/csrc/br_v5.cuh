@@ -45,6 +45,7 @@ struct V5 {
   static constexpr int COLS = CIDX * 4;             // TMEM columns per slab (128)
   static constexpr int NSLOT = 3;                   // slabs resident in TMEM
   static constexpr int TWCOL = NSLOT * COLS;        // lane twiddles: columns 384..447
+  static constexpr int TW4COL = TWCOL + 64;         // split-inverse twiddles: columns 448..479
   static constexpr int UB = R * P * L;              // double2 per gate: U / V / transpose tiles (32 KB)
   static constexpr int XCHG = 2 * 2 * (P / 2) * 32; // u32 per gate: digit swap between level-warps
   static constexpr int SLAB = CIDX * 128 * 16;      // key bytes per step (64 KB)
@@ -57,6 +58,19 @@ struct V5 {
 // o = accumulator component, r = gadget row), tmem lane = 32*w + lane.
 __host__ __device__ __forceinline__ size_t v5_index(int i, int cidx, int tlane) {
   return ((size_t)i * V5::CIDX + cidx) * 128 + tlane;
+}
+
+// Inverse phase split over all four warps of a gate (bit GC-1 set: on at that GC):
+// warp o inverts half (o & 1) of component (o >> 1) with 8 values per lane,
+// instead of two warps inverting a whole component each (the other two idle).
+#ifndef GW_V5_I4
+#define GW_V5_I4 1  // GC = 1 only: same-box A/B 6.52k -> 5.81k cycles per step at GC = 1, +2 % at GC = 2 and 3 (profiles/r02_v5_i4_ab.txt)
+#endif
+// Position of E_h[k1][a'] inside a half of a U row (split inverse): row 2a' + (k1 >> 3),
+// slot 8h + ((k1 & 7) ^ a') -- conflict-free for the writers (lane = 16h + k1, fixed a')
+// and the readers (lane = 16g + a, k1 = 2k' + g, fixed k', h).
+__device__ __forceinline__ int i4_off(int k1, int h, int a2) {
+  return (2 * a2 + (k1 >> 3)) * V5::L + 8 * h + ((k1 & 7) ^ a2);
 }
 
 #ifndef GW_V5_LREG2
@@ -124,9 +138,19 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
   const uint32_t tm_base = *tm_slot;
   const uint32_t tm_warp = tm_base + ((uint32_t)(32 * o) << 16);
   const uint32_t tm_tw = tm_warp + (uint32_t)V5::TWCOL;
+  constexpr bool I4 = (GW_V5_I4 >> (GC - 1)) & 1;
+  const uint32_t tm_tw4 = tm_warp + (uint32_t)V5::TW4COL;
   if (gl == 0 && warp < 4 * GC) {
 #pragma unroll
     for (int k1 = 0; k1 < P; ++k1) tm_st4(tm_tw + (uint32_t)(4 * k1), __ldg(a.tables + 2 * G::TILE + k1 * L + l));
+    if constexpr (I4) {
+      // split inverse, sub-partition o (half b = o & 1), lane 16g + a:
+      // tw'(k1 = 2k' + g, l = b + 2a) for k' = 0..7
+      const int b = o & 1, gg = lane >> 4, aa = lane & 15;
+#pragma unroll
+      for (int k2 = 0; k2 < 8; ++k2)
+        tm_st4(tm_tw4 + (uint32_t)(4 * k2), __ldg(a.tables + 2 * G::TILE + (2 * k2 + gg) * L + b + 2 * aa));
+    }
     tm_wait_st();
   }
 
@@ -311,9 +335,61 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
       mark(2);
       named_barrier(bar_id, 128);  // V complete
       mark(3);
+      // ---------------- I: split inverse, warp o -> half (o & 1) of component (o >> 1) ----------------
+      if constexpr (I4) {
+        const int oo = o >> 1, b = o & 1;
+        double2* tile = U + (size_t)oo * P * L;
+        double2* half = tile + (b << 4);
+        // step A, lane (h, k1): E_h[k1][a'] = DFT-8 over c' of V_b[k1][2c' + h]
+        const int k1 = lane & 15, h = lane >> 4;
+        double2 x[8];
+#pragma unroll
+        for (int c2 = 0; c2 < 8; ++c2) x[bitrev_c<3>(c2)] = tile[(2 * c2 + h) * L + v3_slot(k1, b)];
+        dit<8, -1>(x);
+        __syncwarp();
+#pragma unroll
+        for (int a2 = 0; a2 < 8; ++a2) half[i4_off(k1, h, a2)] = x[a2];
+        __syncwarp();
+        // step B, lane (g, a): S[k1][a] = (E_0 + w16^-a E_1)[k1][a mod 8] conj(tw'(k1, b + 2a)),
+        // k1 = 2k' + g; F_g = DFT-8 over k'; then the radix-2 across lanes g = 0 / 1
+        const int gp = h, aa = k1;  // lane = 16 gp + aa
+        uint32_t tw4[32];
+        tm_ld_raw<32>(tm_tw4, tw4);
+        const double2 wa = c_root64[4 * aa];  // w16^a (conjugated below)
+        double2 e[8][2];
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) e[k2][hh] = half[i4_off(2 * k2 + gp, hh, aa & 7)];
+        tm_wait_ld();
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) {
+          const double2 t = cadd(e[k2][0], cmulc(e[k2][1], wa));
+          const uint32_t* w4 = tw4 + 4 * k2;
+          const double2 tw = make_double2(__hiloint2double(w4[1], w4[0]), __hiloint2double(w4[3], w4[2]));
+          x[bitrev_c<3>(k2)] = cmulc(t, tw);
+        }
+        dit<8, -1>(x);
+        const double sgn = gp ? -1.0 : 1.0;
+        if (active) {
+          uint32_t* Ac = acc_g + oo * N;
+#pragma unroll
+          for (int m2 = 0; m2 < 8; ++m2) {
+            const double2 mine = cmulc(x[m2], c_root64[4 * m2 * gp]);  // gp = 1: w16^-m' F_1
+            const double2 recv = shfl_xor_c(mine, 16);
+            const double2 y = make_double2(fma(sgn, mine.x, recv.x), fma(sgn, mine.y, recv.y));
+            const int m1 = m2 + 8 * gp;
+            const double2 v = cmulc(y, c_root64[G::CSTEP * m1]);  // untwist
+            const uint32_t j = (uint32_t)(L * m1 + b + 2 * aa);
+            if constexpr (PROBE) worst = fmax(worst, fmax(fabs(v.x - rint(v.x)), fabs(v.y - rint(v.y))));
+            Ac[j] += round_mod32(v.x);
+            Ac[j + M] += round_mod32(v.y);
+          }
+        }
+      }
       // ---------------- I: output oo = component oo, two warps per gate ----------------
       const int isel = (i + gl) & 1;  // which warp pair inverts this step
-      if ((o >> 1) == isel) {
+      if (!I4 && (o >> 1) == isel) {
         const int oo = o & 1;
         double2 x[P];
         double2* tile = U + (size_t)oo * P * L;
