@@ -18,8 +18,9 @@ inputs of SURVEY.md Appendix A.  With N GPUs every rank evaluates its own
                 buffers: H2D of both operand matrices + D2H of the result
                 inside the timed region (wall clock, max over ranks).
 * roofline   -- the blind-rotation kernel against the FP64 pipe: algorithmic
-                FLOPs (249,856 n per bootstrap) / its live
-                event-timed duration, vs the DFMA peak measured on this pool.
+                FLOPs of the kernel that ran (v5: 171,008 n per bootstrap; the
+                split-key v3 of exact mode: SURVEY.md §8(d)'s 249,856 n) / its
+                live event-timed duration, vs the DFMA peak measured on this pool.
 * cpu_baseline / --impl reference -- the UNMODIFIED reference (numba,
                 pip-installed into baseline/_ref) through its own
                 runtime.evaluate on all host cores ("reference"); the C
@@ -344,7 +345,8 @@ def config2_latency(ks, P, eng, repeats: int = 3):
         ok = all(C.bits_to_value(decrypt_rows(ks.lwe_sk, outs[k])) == v for k, v in plain.items())
         res[name] = {"app_latency_s": statistics.median(lat), "gates": len(c.gates),
                      "bootstraps": met.bootstrap_count, "levels": len(sched.waves),
-                     "device_time_s": met.device_time_seconds, "decrypt_ok": ok}
+                     "device_time_s": met.device_time_seconds, "wall_runs_s": lat,
+                     "evaluate_wall_s": met.wall_time_seconds, "decrypt_ok": ok}
     res["total_app_latency_s"] = sum(v["app_latency_s"] for v in res.values())
     return res
 
@@ -443,15 +445,27 @@ def run_ours(args):
     br_ms, br_items = stages["blind_rotate"]
     ks_ms, ks_items = stages["keyswitch"]
     launches_br = args.steps
-    flops_per_bootstrap = 249_856 * P.n                      # SURVEY.md §8(d), FP64 path
+    # Algorithmic FP64 work of the kernel that ran (SURVEY.md §8(d) counting: 5 M log2 M
+    # per complex FFT-M, 8 FLOP per complex MAC; M = 512):
+    #   v5 (default, one key image): 4 fwd + 2 inv FFT-512 + 8 x 512 complex MACs = 171,008 per step
+    #   v3 (exact mode, 16-bit split key): 4 fwd + 4 inv + 16 x 512 = 249,856 per step
+    exact = eng.exact()
+    flops_per_step = 249_856 if exact else 171_008
+    flops_per_bootstrap = flops_per_step * P.n
     achieved = flops_per_bootstrap * br_items / (br_ms / 1e3) / 1e12 if br_ms > 0 else 0.0
-    bk_bytes = P.n * 2 * (2 * P.l) * 2 * (P.N // 2) * 16    # FFT-domain key, one pass
-    # the kernel the engine launches for this batch (gw_api.cu launch_v3: gates per CTA
-    # minimising waves x measured step time; loader-warp key streaming below 4 per CTA)
+    cidx = 64 if exact else 32                               # key complexes per TMEM lane and step
+    bk_bytes = P.n * cidx * 128 * 16                         # FFT-domain key image, one pass
+    # the kernel the engine launches for this batch (gw_api.cu launch_v5 / launch_v3: gates
+    # per CTA minimising waves x measured step time)
     sms = torch.cuda.get_device_properties(local).multi_processor_count
-    step_kcyc = {1: 7.8, 2: 9.6, 3: 12.6, 4: 17.7}   # gw_api.cu launch_v3 policy
-    gc = min(step_kcyc, key=lambda g: (-(-G // (sms * g)) * step_kcyc[g], g))
-    kname = f"k_blind_rotate_v3<{gc}, {0 if gc == 4 else 2}, false>"
+    if exact:
+        step_kcyc = {1: 7.8, 2: 9.2, 3: 12.6, 4: 17.7}   # gw_api.cu launch_v3 policy
+        gc = min(step_kcyc, key=lambda g: (-(-G // (sms * g)) * step_kcyc[g], g))
+        kname = f"k_blind_rotate_v3<{gc}, {0 if gc == 4 else 2}, false>"
+    else:
+        step_kcyc = {1: 5.80, 2: 8.04, 3: 10.33}          # gw_api.cu launch_v5 policy
+        gc = min(step_kcyc, key=lambda g: (-(-G // (sms * g)) * step_kcyc[g], g))
+        kname = f"k_blind_rotate_v5<{gc}, false>"
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")) as f:
@@ -466,6 +480,11 @@ def run_ours(args):
                 "kernel": kname,
                 "per_launch_ms": br_ms / launches_br,
                 "work_per_launch": f"{G} bootstraps x {flops_per_bootstrap} FLOP",
+                "flop_count": ("v3 split key: 4 fwd + 4 inv FFT-512 + 16 x 512 complex MACs per step"
+                               if exact else
+                               "v5 one key image: 4 fwd + 2 inv FFT-512 + 8 x 512 complex MACs per step"),
+                "frac_in_split_key_flops": 249_856 * P.n * br_items / (br_ms / 1e3) / 1e12 / FP64_PEAK_TFLOPS
+                if br_ms > 0 else 0.0,
                 "kernel_share_of_step": br_ms / max(sum(step_ms), 1e-9),
                 "keyswitch_ms_per_launch": ks_ms / launches_br,
                 "bk_stream_gbs": bk_bytes / (br_ms / launches_br / 1e3) / 1e9,
@@ -491,7 +510,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         wms = e0.elapsed_time(e1) / 3
         wide = {"gates": Gw, "ms": wms, "gates_per_s": Gw / (wms / 1e3),
-                "fp64_frac": 157_409_280 * Gw / (wms / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
+                "fp64_frac": flops_per_bootstrap * Gw / (wms / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
                 "note": "device-resident NAND batch, 3 gates per SM (the netlists' wide levels)"}
         del opsw, outw
 

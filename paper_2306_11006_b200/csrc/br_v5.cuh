@@ -73,6 +73,14 @@ __device__ __forceinline__ int i4_off(int k1, int h, int a2) {
   return (2 * a2 + (k1 >> 3)) * V5::L + 8 * h + ((k1 & 7) ^ a2);
 }
 
+// Stagger (bit GC-1): gate 1 starts after gate 0's F(0), gate 2 after its M(0).
+#ifndef GW_V5_STAGGER
+#define GW_V5_STAGGER 0  // same-box A/B: off is 1.9 % faster at GC = 2 (8.04k vs 8.19k) and 2.8 % at GC = 3 (profiles/r02_v5_stagger_ab.txt)
+#endif
+// Loader warps poll the slot they refill with a nanosleep back-off (ns; 0 = spin).
+#ifndef GW_V5_LDR_SLEEP
+#define GW_V5_LDR_SLEEP 0
+#endif
 #ifndef GW_V5_LREG2
 #define GW_V5_LREG2 64
 #endif
@@ -208,7 +216,11 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
       }
 #endif
       if (i >= NSLOT) {
+#if GW_V5_LDR_SLEEP
+        mbar_wait_backoff(&empty_bar[slot], (uint32_t)(((i - NSLOT) / NSLOT) & 1), GW_V5_LDR_SLEEP);
+#else
         mbar_wait(&empty_bar[slot], (uint32_t)(((i - NSLOT) / NSLOT) & 1));
+#endif
         tm_fence_after();
       }
       const uint32_t dst = tm_warp + (uint32_t)(slot * COLS);
@@ -229,7 +241,7 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
   } else {
     if constexpr (GC >= 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(CREG));
     // stagger (as v3): gate 1 starts after gate 0's F(0), gate 2 after its M(0)
-    constexpr bool kStagger = GC >= 2;
+    constexpr bool kStagger = GC >= 2 && ((GW_V5_STAGGER >> (GC - 1)) & 1);
     if (kStagger && gl >= 1) mbar_wait(&go_bar[gl - 1], 0);
     uint32_t a_next = lin_at(0);
     double worst = 0.0;  // PROBE only
