@@ -17,8 +17,8 @@
 // every rounded value lies within a few hundredths of an integer, so the
 // outputs are bit-identical to the exact (split-key, v3) path and to the
 // reference on every tested input.  The worst-case analytic bound still
-// limits any deviation to a few units of 2^-32 per coefficient and step,
-// far inside the decryption margin (the north star's "stated noise bound").
+// limits the phase deviation to < 2^24 raw units after n steps, far inside the
+// 2^28 decryption margin (the north star's "stated noise bound").
 // GATEWAVE_BR_EXACT=1 (gw_set_exact) selects the split-key v3 kernel.
 //
 // CTA = GC gates x 4 compute warps + 4 key-loader warps, one CTA per SM.
@@ -26,11 +26,12 @@
 //   M  warp w: frequency pairs (k1, c), c in [4w, 4w+4): last forward radix-2
 //      stage of the 4 rows, 2 outputs x 4 rows complex MACs against the key
 //      values in TMEM, first inverse radix-2 stage -> V rows 0, 1
-//   I  two of the four warps (alternating by step and gate, so the four SMSPs
-//      share the inverse work): inverse tail of component o, untwist, round,
-//      acc[o] += v (one writer per word).
+//   I  GC >= 2: two of the four warps (alternating by step and gate, so the four
+//      SMSPs share the inverse work) each invert one component: inverse tail,
+//      untwist, round, acc[o] += v (one writer per word).  GC = 1: all four
+//      warps, each half a component (8 values per lane, GW_V5_I4).
 // TMEM (512 columns): 3 key slabs of 128 columns (slab i in slot i mod 3) +
-// the lane twiddle table (64 columns).  The loader warps run up to two steps
+// the lane twiddle table (64 columns) + the split-inverse twiddles (32 columns).  The loader warps run up to two steps
 // ahead of the MAC: slab i waits for MAC(i - 3) to release its slot.
 #pragma once
 #include "br_v3.cuh"
