@@ -75,6 +75,12 @@ __device__ __forceinline__ int i4_off(int k1, int h, int a2) {
 }
 
 // Stagger (bit GC-1): gate 1 starts after gate 0's F(0), gate 2 after its M(0).
+#ifndef GW_V5_STAGGER_AT2
+#define GW_V5_STAGGER_AT2 0
+#endif
+#ifndef GW_V5_RED
+#define GW_V5_RED 1  // accumulator updates as shared-memory RED.ADD (same-box A/B: -0.4 / -0.7 / -1 % at GC = 1 / 2 / 3 vs load-add-store, profiles/r02_v5_stagger_red_ab.txt)
+#endif
 #ifndef GW_V5_STAGGER
 #define GW_V5_STAGGER 0  // same-box A/B: off is 1.9 % faster at GC = 2 (8.04k vs 8.19k) and 2.8 % at GC = 3 (profiles/r02_v5_stagger_ab.txt)
 #endif
@@ -243,7 +249,8 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
     if constexpr (GC >= 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(CREG));
     // stagger (as v3): gate 1 starts after gate 0's F(0), gate 2 after its M(0)
     constexpr bool kStagger = GC >= 2 && ((GW_V5_STAGGER >> (GC - 1)) & 1);
-    if (kStagger && gl >= 1) mbar_wait(&go_bar[gl - 1], 0);
+    // GC = 2: gate 1 waits for gate 0's F(0) (GW_V5_STAGGER_AT2 = 0) or M(0) (1)
+    if (kStagger && gl >= 1) mbar_wait(&go_bar[GC == 2 ? GW_V5_STAGGER_AT2 : gl - 1], 0);
     uint32_t a_next = lin_at(0);
     double worst = 0.0;  // PROBE only
     int slot = 0;
@@ -395,8 +402,13 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
             const double2 v = cmulc(y, c_root64[G::CSTEP * m1]);  // untwist
             const uint32_t j = (uint32_t)(L * m1 + b + 2 * aa);
             if constexpr (PROBE) worst = fmax(worst, fmax(fabs(v.x - rint(v.x)), fabs(v.y - rint(v.y))));
+#if GW_V5_RED
+            atomicAdd(Ac + j, round_mod32(v.x));
+            atomicAdd(Ac + j + M, round_mod32(v.y));
+#else
             Ac[j] += round_mod32(v.x);
             Ac[j + M] += round_mod32(v.y);
+#endif
           }
         }
       }
@@ -416,8 +428,13 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
             const double2 v = m1 == 0 ? x[0] : cmulc(x[m1], c_root64[G::CSTEP * m1]);
             const uint32_t j = (uint32_t)(L * m1 + l);
             if constexpr (PROBE) worst = fmax(worst, fmax(fabs(v.x - rint(v.x)), fabs(v.y - rint(v.y))));
+#if GW_V5_RED
+            atomicAdd(Ac + j, round_mod32(v.x));
+            atomicAdd(Ac + j + M, round_mod32(v.y));
+#else
             Ac[j] += round_mod32(v.x);
             Ac[j + M] += round_mod32(v.y);
+#endif
           }
         }
       }

@@ -1,0 +1,3 @@
+# A/B: stagger point at GC=2 (none / after F(0) / after M(0)), RED accumulator updates
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+for rep in 1 2; do for v in base stF stM red; do echo "== $v"; GATEWAVE_B200_LIB=variants/lib_$v.so timeout 300 python tools/br_time.py 148 256 444; done; done
