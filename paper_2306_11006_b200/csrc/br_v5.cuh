@@ -75,6 +75,14 @@ __device__ __forceinline__ int i4_off(int k1, int h, int a2) {
 }
 
 // Stagger (bit GC-1): gate 1 starts after gate 0's F(0), gate 2 after its M(0).
+// Paired split inverse (bit GC-1, GC <= 2; takes precedence over GW_V5_I4): two warps
+// invert one component together, each doing the odd or even outputs of both DFT-16
+// passes (DIF split, 8 values per lane), with the lane twiddles applied by the writer
+// of the transpose.  GC = 2: the pair is warp o of gate 0 and warp o of gate 1 (one
+// SMSP), inverting component o & 1 of gate o >> 1; GC = 1: warps (0, 1) and (2, 3).
+#ifndef GW_V5_IPAIR
+#define GW_V5_IPAIR 1  // GC = 1: 5.78k -> 5.37k cycles per step; GC = 2: +3 % (profiles/r02_v5_ipair_ab.txt)
+#endif
 #ifndef GW_V5_STAGGER_AT2
 #define GW_V5_STAGGER_AT2 0
 #endif
@@ -153,7 +161,8 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
   const uint32_t tm_base = *tm_slot;
   const uint32_t tm_warp = tm_base + ((uint32_t)(32 * o) << 16);
   const uint32_t tm_tw = tm_warp + (uint32_t)V5::TWCOL;
-  constexpr bool I4 = (GW_V5_I4 >> (GC - 1)) & 1;
+  constexpr bool IPAIR = GC <= 2 && ((GW_V5_IPAIR >> (GC - 1)) & 1);
+  constexpr bool I4 = !IPAIR && ((GW_V5_I4 >> (GC - 1)) & 1);
   const uint32_t tm_tw4 = tm_warp + (uint32_t)V5::TW4COL;
   if (gl == 0 && warp < 4 * GC) {
 #pragma unroll
@@ -165,6 +174,16 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
 #pragma unroll
       for (int k2 = 0; k2 < 8; ++k2)
         tm_st4(tm_tw4 + (uint32_t)(4 * k2), __ldg(a.tables + 2 * G::TILE + (2 * k2 + gg) * L + b + 2 * aa));
+    }
+    if constexpr (IPAIR) {
+      // paired inverse, writer lane (k1, b) of role e: tw'(k1, b + 2 (2a' + e)), a' = 0..7
+      // (both roles' tables in every sub-partition: columns TW4COL + 32 e)
+      const int k1 = lane >> 1, b = lane & 1;
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int a2 = 0; a2 < 8; ++a2)
+          tm_st4(tm_tw4 + (uint32_t)(32 * e + 4 * a2), __ldg(a.tables + 2 * G::TILE + k1 * L + b + 2 * (2 * a2 + e)));
     }
     tm_wait_st();
   }
@@ -353,9 +372,74 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
       if (lane == 0) mbar_arrive(&empty_bar[slot]);
       if (kStagger && i == 0 && gl == 0 && lane == 0) mbar_arrive(&go_bar[1]);
       mark(2);
-      named_barrier(bar_id, 128);  // V complete
+      // V complete (paired inverse at GC = 2: the pairs span both gates)
+      if (IPAIR && GC == 2) named_barrier(13, 128 * GC); else named_barrier(bar_id, 128);
       mark(3);
       // ---------------- I: split inverse, warp o -> half (o & 1) of component (o >> 1) ----------------
+      if constexpr (IPAIR) {
+        // pair q inverts component oo of gate tg; role rr: even (0) / odd (1) outputs
+        const int rr = GC == 2 ? gl : (o & 1);
+        const int tg = GC == 2 ? (o >> 1) : gl;
+        const int oo = GC == 2 ? (o & 1) : (o >> 1);
+        const int pair_bar = 9 + (GC == 2 ? o : (o >> 1));
+        double2* Ut = ubuf_all + (size_t)tg * UB;
+        const double2* tileV = Ut + (size_t)oo * P * L;
+        double2* scratch = Ut + (size_t)(2 + oo) * P * L;   // rows 2, 3 are free after M
+        const bool act_t = (int)blockIdx.x * GC + tg < a.B;
+        uint32_t tw8[32];
+        tm_ld_raw<32>(tm_tw4 + (uint32_t)(32 * rr), tw8);
+        // pass 1, lane (k1, b): T[2a' + rr] = DFT-8_{c'} of (V[c'] +- V[c'+8]) w16^(-rr c')
+        double2 x[8];
+        {
+          double2 v[16];
+#pragma unroll
+          for (int c = 0; c < P; ++c) v[c] = tileV[c * L + pos];
+#pragma unroll
+          for (int c2 = 0; c2 < 8; ++c2)
+            x[bitrev_c<3>(c2)] = rr == 0 ? cadd(v[c2], v[c2 + 8])
+                                          : (c2 == 0 ? csub(v[0], v[8]) : cmulc(csub(v[c2], v[c2 + 8]), c_root64[4 * c2]));
+        }
+        dit<8, -1>(x);
+        tm_wait_ld();
+        {
+          const int k1 = l >> 1, b = l & 1;
+#pragma unroll
+          for (int a2 = 0; a2 < 8; ++a2) {
+            const uint32_t* w4 = tw8 + 4 * a2;
+            const double2 tw = make_double2(__hiloint2double(w4[1], w4[0]), __hiloint2double(w4[3], w4[2]));
+            scratch[k1 * L + swz(k1, b + 2 * (2 * a2 + rr))] = cmulc(x[a2], tw);
+          }
+        }
+        named_barrier(pair_bar, 64);
+        // pass 2, lane l: z[2m' + rr] = DFT-8_{k'} of (S[k'] +- S[k'+8]) w16^(-rr k')
+        {
+          double2 v[16];
+#pragma unroll
+          for (int k1 = 0; k1 < P; ++k1) v[k1] = scratch[k1 * L + swz(k1, l)];
+#pragma unroll
+          for (int k2 = 0; k2 < 8; ++k2)
+            x[bitrev_c<3>(k2)] = rr == 0 ? cadd(v[k2], v[k2 + 8])
+                                          : (k2 == 0 ? csub(v[0], v[8]) : cmulc(csub(v[k2], v[k2 + 8]), c_root64[4 * k2]));
+        }
+        dit<8, -1>(x);
+        if (act_t) {
+          uint32_t* Ac = acc_all + (size_t)tg * 2 * N + oo * N;
+#pragma unroll
+          for (int m2 = 0; m2 < 8; ++m2) {
+            const int m1 = 2 * m2 + rr;
+            const double2 v = m1 == 0 ? x[0] : cmulc(x[m2], c_root64[G::CSTEP * m1]);  // untwist
+            const uint32_t j = (uint32_t)(L * m1 + l);
+            if constexpr (PROBE) worst = fmax(worst, fmax(fabs(v.x - rint(v.x)), fabs(v.y - rint(v.y))));
+#if GW_V5_RED
+            atomicAdd(Ac + j, round_mod32(v.x));
+            atomicAdd(Ac + j + M, round_mod32(v.y));
+#else
+            Ac[j] += round_mod32(v.x);
+            Ac[j + M] += round_mod32(v.y);
+#endif
+          }
+        }
+      }
       if constexpr (I4) {
         const int oo = o >> 1, b = o & 1;
         double2* tile = U + (size_t)oo * P * L;
@@ -414,7 +498,7 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
       }
       // ---------------- I: output oo = component oo, two warps per gate ----------------
       const int isel = (i + gl) & 1;  // which warp pair inverts this step
-      if (!I4 && (o >> 1) == isel) {
+      if (!I4 && !IPAIR && (o >> 1) == isel) {
         const int oo = o & 1;
         double2 x[P];
         double2* tile = U + (size_t)oo * P * L;
@@ -439,7 +523,8 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
         }
       }
       mark(4);
-      named_barrier(bar_id, 128);  // acc updated before the next decomposition
+      // acc updated before the next decomposition
+      if (IPAIR && GC == 2) named_barrier(13, 128 * GC); else named_barrier(bar_id, 128);
       mark(5);
       slot = slot + 1 == NSLOT ? 0 : slot + 1;
     }
