@@ -68,6 +68,8 @@ def _args():
     ap.add_argument("--gates", type=int, default=GATES)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-netlist", action="store_true")
+    ap.add_argument("--sharded-timeout", type=float, default=1200.0,
+                    help="deadline (s) for the sharded netlists at N > 1; on expiry the line is printed without them")
     ap.add_argument("--sharded", default="auto",
                     help="netlists evaluated sharded over the GPUs: auto (config4 at N>1, + config5 at "
                          "N=8), none, or a comma list of config4,config5,config3")
@@ -568,20 +570,6 @@ def run_ours(args):
     if not args.no_netlist and ws == 1:
         netlist = config2_latency(ks, P, eng)
 
-    # ---- netlists sharded over the GPUs (config 4; config 5 at N = 8) --------
-    sharded = None
-    if not args.no_netlist and args.sharded != "none":
-        which = ([] if ws == 1 else ["config4"] + (["config5"] if ws == 8 else [])) \
-            if args.sharded == "auto" else [x for x in args.sharded.split(",") if x]
-        if which:
-            sharded = {}
-            for name in which:
-                # a failure here must not cost the config-1 line: report it instead
-                try:
-                    sharded[name] = netlist_sharded(name, ks, P, dist, rank, ws)
-                except Exception as e:  # noqa: BLE001
-                    sharded[name] = {"error": f"{type(e).__name__}: {e}"[:500]}
-
     # ---- CPU baseline: the unmodified reference, rank 0 at N=1 only ---------
     cpu = cpu_c2 = cpu_c345 = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -617,12 +605,42 @@ def run_ours(args):
             "app_latency_config2": netlist,
             "app_latency_config2_cpu": cpu_c2,
             "cpu_netlists_extrapolated": cpu_c345,
-            "netlists_sharded": sharded,
+            "netlists_sharded": None,
             "throughput_wide_level": wide,
             "param110": p110,
             "clocks": clk.summary(),
             "parity": parity,
         }
+    # ---- netlists sharded over the GPUs (config 4; config 5 at N = 8) --------
+    # Run last, under a deadline: a stuck collective must not cost the config-1 line.
+    # On expiry rank 0 prints the line with the timeout recorded and every rank exits 0.
+    which = []
+    if not args.no_netlist and args.sharded != "none":
+        which = ([] if ws == 1 else ["config4"] + (["config5"] if ws == 8 else [])) \
+            if args.sharded == "auto" else [x for x in args.sharded.split(",") if x]
+    if which:
+        sharded = {}
+
+        def _deadline():
+            if rank == 0:
+                sharded["error"] = f"timeout after {args.sharded_timeout:.0f} s (completed: {sorted(sharded)})"
+                line["netlists_sharded"] = sharded
+                print(json.dumps(line), flush=True)
+            os._exit(0)
+
+        timer = threading.Timer(args.sharded_timeout, _deadline)
+        timer.daemon = True
+        timer.start()
+        for name in which:
+            # a failure here must not cost the config-1 line: report it instead
+            try:
+                sharded[name] = netlist_sharded(name, ks, P, dist, rank, ws)
+            except Exception as e:  # noqa: BLE001
+                sharded[name] = {"error": f"{type(e).__name__}: {e}"[:500]}
+        timer.cancel()
+        if rank == 0:
+            line["netlists_sharded"] = sharded
+    if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
