@@ -81,7 +81,12 @@ __device__ __forceinline__ int i4_off(int k1, int h, int a2) {
 // of the transpose.  GC = 2: the pair is warp o of gate 0 and warp o of gate 1 (one
 // SMSP), inverting component o & 1 of gate o >> 1; GC = 1: warps (0, 1) and (2, 3).
 #ifndef GW_V5_IPAIR
-#define GW_V5_IPAIR 1  // GC = 1: 5.78k -> 5.37k cycles per step; GC = 2: +3 % (profiles/r02_v5_ipair_ab.txt)
+#define GW_V5_IPAIR 7  // every GC, pairs within a gate: GC = 1 5.78k -> 5.37k (profiles/r02_v5_ipair_ab.txt), GC = 2 7.99k -> 7.61k, GC = 3 10.40k -> 10.07k (profiles/r02_v5_ipair_gc23_ab.txt)
+#endif
+// GC = 2 pairs: 0 = within a gate (warps (0,1) / (2,3) of each gate, per-gate barriers),
+// 1 = across the gates (warp o of gate 0 with warp o of gate 1, CTA-wide barriers)
+#ifndef GW_V5_IPAIR_CROSS
+#define GW_V5_IPAIR_CROSS 0
 #endif
 #ifndef GW_V5_STAGGER_AT2
 #define GW_V5_STAGGER_AT2 0
@@ -161,7 +166,8 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
   const uint32_t tm_base = *tm_slot;
   const uint32_t tm_warp = tm_base + ((uint32_t)(32 * o) << 16);
   const uint32_t tm_tw = tm_warp + (uint32_t)V5::TWCOL;
-  constexpr bool IPAIR = GC <= 2 && ((GW_V5_IPAIR >> (GC - 1)) & 1);
+  constexpr bool IPAIR = ((GW_V5_IPAIR >> (GC - 1)) & 1) != 0;
+  constexpr bool IPX = IPAIR && GC == 2 && GW_V5_IPAIR_CROSS;  // pairs across the two gates of a CTA
   constexpr bool I4 = !IPAIR && ((GW_V5_I4 >> (GC - 1)) & 1);
   const uint32_t tm_tw4 = tm_warp + (uint32_t)V5::TW4COL;
   if (gl == 0 && warp < 4 * GC) {
@@ -373,15 +379,17 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
       if (kStagger && i == 0 && gl == 0 && lane == 0) mbar_arrive(&go_bar[1]);
       mark(2);
       // V complete (paired inverse at GC = 2: the pairs span both gates)
-      if (IPAIR && GC == 2) named_barrier(13, 128 * GC); else named_barrier(bar_id, 128);
+      if (IPX) named_barrier(13, 128 * GC); else named_barrier(bar_id, 128);
       mark(3);
       // ---------------- I: split inverse, warp o -> half (o & 1) of component (o >> 1) ----------------
       if constexpr (IPAIR) {
         // pair q inverts component oo of gate tg; role rr: even (0) / odd (1) outputs
-        const int rr = GC == 2 ? gl : (o & 1);
-        const int tg = GC == 2 ? (o >> 1) : gl;
-        const int oo = GC == 2 ? (o & 1) : (o >> 1);
-        const int pair_bar = 9 + (GC == 2 ? o : (o >> 1));
+        const int rr = IPX ? gl : (o & 1);
+        const int tg = IPX ? (o >> 1) : gl;
+        const int oo = IPX ? (o & 1) : (o >> 1);
+        // named barrier ids: B1-B3 use 1..GC, the F level pairs 5..4+2GC
+        const int pq = 2 * gl + (o >> 1);
+        const int pair_bar = IPX ? 9 + o : GC == 3 ? (pq == 0 ? 4 : 10 + pq) : 9 + pq;
         double2* Ut = ubuf_all + (size_t)tg * UB;
         const double2* tileV = Ut + (size_t)oo * P * L;
         double2* scratch = Ut + (size_t)(2 + oo) * P * L;   // rows 2, 3 are free after M
@@ -524,7 +532,7 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
       }
       mark(4);
       // acc updated before the next decomposition
-      if (IPAIR && GC == 2) named_barrier(13, 128 * GC); else named_barrier(bar_id, 128);
+      if (IPX) named_barrier(13, 128 * GC); else named_barrier(bar_id, 128);
       mark(5);
       slot = slot + 1 == NSLOT ? 0 : slot + 1;
     }
