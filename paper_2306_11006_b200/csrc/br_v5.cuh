@@ -26,13 +26,13 @@
 //   M  warp w: frequency pairs (k1, c), c in [4w, 4w+4): last forward radix-2
 //      stage of the 4 rows, 2 outputs x 4 rows complex MACs against the key
 //      values in TMEM, first inverse radix-2 stage -> V rows 0, 1
-//   I  GC >= 2: two of the four warps (alternating by step and gate, so the four
-//      SMSPs share the inverse work) each invert one component: inverse tail,
-//      untwist, round, acc[o] += v (one writer per word).  GC = 1: all four
-//      warps, each half a component (8 values per lane, GW_V5_I4).
-// TMEM (512 columns): 3 key slabs of 128 columns (slab i in slot i mod 3) +
-// the lane twiddle table (64 columns) + the split-inverse twiddles (32 columns).  The loader warps run up to two steps
-// ahead of the MAC: slab i waits for MAC(i - 3) to release its slot.
+//   I  warps (2c, 2c + 1) invert component c together (the paired inverse below:
+//      each computes the even or odd outputs of both DFT-16 passes), untwist,
+//      round, acc[c] += v with shared-memory RED.ADD.
+// TMEM (512 columns): 3 key slabs of 128 columns (slab i in slot i mod 3), the
+// forward lane twiddle table (64 columns) and the paired inverse's writer-side
+// twiddles (2 x 32 columns).  The loader warps run up to two steps ahead of the
+// MAC: slab i waits for MAC(i - 3) to release its slot.
 #pragma once
 #include "br_v3.cuh"
 
@@ -46,7 +46,7 @@ struct V5 {
   static constexpr int COLS = CIDX * 4;             // TMEM columns per slab (128)
   static constexpr int NSLOT = 3;                   // slabs resident in TMEM
   static constexpr int TWCOL = NSLOT * COLS;        // lane twiddles: columns 384..447
-  static constexpr int TW4COL = TWCOL + 64;         // split-inverse twiddles: columns 448..479
+  static constexpr int TW4COL = TWCOL + 64;         // paired-inverse twiddles: columns 448..511
   static constexpr int UB = R * P * L;              // double2 per gate: U / V / transpose tiles (32 KB)
   static constexpr int XCHG = 2 * 2 * (P / 2) * 32; // u32 per gate: digit swap between level-warps
   static constexpr int SLAB = CIDX * 128 * 16;      // key bytes per step (64 KB)
@@ -61,46 +61,20 @@ __host__ __device__ __forceinline__ size_t v5_index(int i, int cidx, int tlane) 
   return ((size_t)i * V5::CIDX + cidx) * 128 + tlane;
 }
 
-// Inverse phase split over all four warps of a gate (bit GC-1 set: on at that GC):
-// warp o inverts half (o & 1) of component (o >> 1) with 8 values per lane,
-// instead of two warps inverting a whole component each (the other two idle).
-#ifndef GW_V5_I4
-#define GW_V5_I4 1  // GC = 1 only: same-box A/B 6.52k -> 5.81k cycles per step at GC = 1, +2 % at GC = 2 and 3 (profiles/r02_v5_i4_ab.txt)
-#endif
-// Position of E_h[k1][a'] inside a half of a U row (split inverse): row 2a' + (k1 >> 3),
-// slot 8h + ((k1 & 7) ^ a') -- conflict-free for the writers (lane = 16h + k1, fixed a')
-// and the readers (lane = 16g + a, k1 = 2k' + g, fixed k', h).
-__device__ __forceinline__ int i4_off(int k1, int h, int a2) {
-  return (2 * a2 + (k1 >> 3)) * V5::L + 8 * h + ((k1 & 7) ^ a2);
-}
-
-// Stagger (bit GC-1): gate 1 starts after gate 0's F(0), gate 2 after its M(0).
-// Paired split inverse (bit GC-1, GC <= 2; takes precedence over GW_V5_I4): two warps
-// invert one component together, each doing the odd or even outputs of both DFT-16
-// passes (DIF split, 8 values per lane), with the lane twiddles applied by the writer
-// of the transpose.  GC = 2: the pair is warp o of gate 0 and warp o of gate 1 (one
-// SMSP), inverting component o & 1 of gate o >> 1; GC = 1: warps (0, 1) and (2, 3).
-#ifndef GW_V5_IPAIR
-#define GW_V5_IPAIR 7  // every GC, pairs within a gate: GC = 1 5.78k -> 5.37k (profiles/r02_v5_ipair_ab.txt), GC = 2 7.99k -> 7.61k, GC = 3 10.40k -> 10.07k (profiles/r02_v5_ipair_gc23_ab.txt)
-#endif
-// GC = 2 pairs: 0 = within a gate (warps (0,1) / (2,3) of each gate, per-gate barriers),
-// 1 = across the gates (warp o of gate 0 with warp o of gate 1, CTA-wide barriers)
-#ifndef GW_V5_IPAIR_CROSS
-#define GW_V5_IPAIR_CROSS 0
-#endif
-#ifndef GW_V5_STAGGER_AT2
-#define GW_V5_STAGGER_AT2 0
-#endif
+// Paired split inverse: two warps of a gate invert one accumulator component together,
+// each doing the odd or even outputs of both DFT-16 passes (decimation in frequency:
+// both read all 16 inputs, form the 8 half-sums or twisted half-differences and run a
+// DFT-8), with the lane twiddles applied by the writer of the transpose.  Warps (0, 1)
+// take component 0, warps (2, 3) component 1.  Same-box A/B (cycles per step):
+// GC = 1 5.78k -> 5.37k, GC = 2 7.99k -> 7.61k, GC = 3 10.40k -> 10.07k against two
+// inverting warps per gate (profiles/r02_v5_ipair_ab.txt, r02_v5_ipair_gc23_ab.txt).
+// Rejected on the same box: four warps on quarter problems with a shuffle radix-2
+// (GC = 1 5.81k), pairs across the two gates of a CTA (GC = 2 8.23k), gate stagger
+// (+1.9-2.8 %), loader nanosleep back-off (+0.7-1.7 % at GC = 2, 3).
 #ifndef GW_V5_RED
 #define GW_V5_RED 1  // accumulator updates as shared-memory RED.ADD (same-box A/B: -0.4 / -0.7 / -1 % at GC = 1 / 2 / 3 vs load-add-store, profiles/r02_v5_stagger_red_ab.txt)
 #endif
-#ifndef GW_V5_STAGGER
-#define GW_V5_STAGGER 0  // same-box A/B: off is 1.9 % faster at GC = 2 (8.04k vs 8.19k) and 2.8 % at GC = 3 (profiles/r02_v5_stagger_ab.txt)
-#endif
-// Loader warps poll the slot they refill with a nanosleep back-off (ns; 0 = spin).
-#ifndef GW_V5_LDR_SLEEP
-#define GW_V5_LDR_SLEEP 0
-#endif
+
 #ifndef GW_V5_LREG2
 #define GW_V5_LREG2 64
 #endif
@@ -125,8 +99,7 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
   uint64_t* bars = reinterpret_cast<uint64_t*>(xchg_all + (size_t)GC * V5::XCHG);
   uint64_t* full_bar = bars;           // [3] the loader warps stored slab i in slot i % 3
   uint64_t* empty_bar = bars + NSLOT;  // [3] every compute warp finished its MAC reads of slot i % 3
-  uint64_t* go_bar = bars + 2 * NSLOT; // [2] stagger: gate 0 reached its start points for gates 1 / 2
-  uint32_t* tm_slot = reinterpret_cast<uint32_t*>(bars + 2 * NSLOT + 2);
+  uint32_t* tm_slot = reinterpret_cast<uint32_t*>(bars + 2 * NSLOT);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, l = lane;
   const int gl = warp >> 2, o = warp & 3;
@@ -155,8 +128,6 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
       mbar_init(&full_bar[k], 4);
       mbar_init(&empty_bar[k], 4 * GC);
     }
-    mbar_init(&go_bar[0], 4);
-    mbar_init(&go_bar[1], 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) tm_alloc(tm_slot, 512);
@@ -166,22 +137,11 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
   const uint32_t tm_base = *tm_slot;
   const uint32_t tm_warp = tm_base + ((uint32_t)(32 * o) << 16);
   const uint32_t tm_tw = tm_warp + (uint32_t)V5::TWCOL;
-  constexpr bool IPAIR = ((GW_V5_IPAIR >> (GC - 1)) & 1) != 0;
-  constexpr bool IPX = IPAIR && GC == 2 && GW_V5_IPAIR_CROSS;  // pairs across the two gates of a CTA
-  constexpr bool I4 = !IPAIR && ((GW_V5_I4 >> (GC - 1)) & 1);
   const uint32_t tm_tw4 = tm_warp + (uint32_t)V5::TW4COL;
   if (gl == 0 && warp < 4 * GC) {
 #pragma unroll
     for (int k1 = 0; k1 < P; ++k1) tm_st4(tm_tw + (uint32_t)(4 * k1), __ldg(a.tables + 2 * G::TILE + k1 * L + l));
-    if constexpr (I4) {
-      // split inverse, sub-partition o (half b = o & 1), lane 16g + a:
-      // tw'(k1 = 2k' + g, l = b + 2a) for k' = 0..7
-      const int b = o & 1, gg = lane >> 4, aa = lane & 15;
-#pragma unroll
-      for (int k2 = 0; k2 < 8; ++k2)
-        tm_st4(tm_tw4 + (uint32_t)(4 * k2), __ldg(a.tables + 2 * G::TILE + (2 * k2 + gg) * L + b + 2 * aa));
-    }
-    if constexpr (IPAIR) {
+    {
       // paired inverse, writer lane (k1, b) of role e: tw'(k1, b + 2 (2a' + e)), a' = 0..7
       // (both roles' tables in every sub-partition: columns TW4COL + 32 e)
       const int k1 = lane >> 1, b = lane & 1;
@@ -248,11 +208,7 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
       }
 #endif
       if (i >= NSLOT) {
-#if GW_V5_LDR_SLEEP
-        mbar_wait_backoff(&empty_bar[slot], (uint32_t)(((i - NSLOT) / NSLOT) & 1), GW_V5_LDR_SLEEP);
-#else
         mbar_wait(&empty_bar[slot], (uint32_t)(((i - NSLOT) / NSLOT) & 1));
-#endif
         tm_fence_after();
       }
       const uint32_t dst = tm_warp + (uint32_t)(slot * COLS);
@@ -272,10 +228,6 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
     }
   } else {
     if constexpr (GC >= 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(CREG));
-    // stagger (as v3): gate 1 starts after gate 0's F(0), gate 2 after its M(0)
-    constexpr bool kStagger = GC >= 2 && ((GW_V5_STAGGER >> (GC - 1)) & 1);
-    // GC = 2: gate 1 waits for gate 0's F(0) (GW_V5_STAGGER_AT2 = 0) or M(0) (1)
-    if (kStagger && gl >= 1) mbar_wait(&go_bar[GC == 2 ? GW_V5_STAGGER_AT2 : gl - 1], 0);
     uint32_t a_next = lin_at(0);
     double worst = 0.0;  // PROBE only
     int slot = 0;
@@ -329,7 +281,6 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
 #pragma unroll
         for (int c = 0; c < P; ++c) tile[c * L + pos] = x[c];
       }
-      if (kStagger && i == 0 && gl == 0 && lane == 0) mbar_arrive(&go_bar[0]);
       mark(0);
       named_barrier(bar_id, 128);  // U complete
       mark(1);
@@ -376,24 +327,18 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
       tm_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[slot]);
-      if (kStagger && i == 0 && gl == 0 && lane == 0) mbar_arrive(&go_bar[1]);
       mark(2);
-      // V complete (paired inverse at GC = 2: the pairs span both gates)
-      if (IPX) named_barrier(13, 128 * GC); else named_barrier(bar_id, 128);
+      named_barrier(bar_id, 128);  // V complete
       mark(3);
-      // ---------------- I: split inverse, warp o -> half (o & 1) of component (o >> 1) ----------------
-      if constexpr (IPAIR) {
-        // pair q inverts component oo of gate tg; role rr: even (0) / odd (1) outputs
-        const int rr = IPX ? gl : (o & 1);
-        const int tg = IPX ? (o >> 1) : gl;
-        const int oo = IPX ? (o & 1) : (o >> 1);
-        // named barrier ids: B1-B3 use 1..GC, the F level pairs 5..4+2GC
-        const int pq = 2 * gl + (o >> 1);
-        const int pair_bar = IPX ? 9 + o : GC == 3 ? (pq == 0 ? 4 : 10 + pq) : 9 + pq;
-        double2* Ut = ubuf_all + (size_t)tg * UB;
-        const double2* tileV = Ut + (size_t)oo * P * L;
-        double2* scratch = Ut + (size_t)(2 + oo) * P * L;   // rows 2, 3 are free after M
-        const bool act_t = (int)blockIdx.x * GC + tg < a.B;
+      // ---------------- I: paired inverse, warps (2 oo, 2 oo + 1) -> component oo ----------------
+      {
+        // warps (2 oo, 2 oo + 1) invert component oo; role rr: even (0) / odd (1) outputs
+        const int rr = o & 1, oo = o >> 1;
+        // named barrier ids: 1..GC per gate (B1-B3), 5..4+2GC the F level pairs
+        const int pq = 2 * gl + oo;
+        const int pair_bar = GC == 3 ? (pq == 0 ? 4 : 10 + pq) : 9 + pq;
+        const double2* tileV = U + (size_t)oo * P * L;
+        double2* scratch = U + (size_t)(2 + oo) * P * L;   // rows 2, 3 are free after M
         uint32_t tw8[32];
         tm_ld_raw<32>(tm_tw4 + (uint32_t)(32 * rr), tw8);
         // pass 1, lane (k1, b): T[2a' + rr] = DFT-8_{c'} of (V[c'] +- V[c'+8]) w16^(-rr c')
@@ -430,8 +375,8 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
                                           : (k2 == 0 ? csub(v[0], v[8]) : cmulc(csub(v[k2], v[k2 + 8]), c_root64[4 * k2]));
         }
         dit<8, -1>(x);
-        if (act_t) {
-          uint32_t* Ac = acc_all + (size_t)tg * 2 * N + oo * N;
+        if (active) {
+          uint32_t* Ac = acc_g + oo * N;
 #pragma unroll
           for (int m2 = 0; m2 < 8; ++m2) {
             const int m1 = 2 * m2 + rr;
@@ -448,91 +393,8 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
           }
         }
       }
-      if constexpr (I4) {
-        const int oo = o >> 1, b = o & 1;
-        double2* tile = U + (size_t)oo * P * L;
-        double2* half = tile + (b << 4);
-        // step A, lane (h, k1): E_h[k1][a'] = DFT-8 over c' of V_b[k1][2c' + h]
-        const int k1 = lane & 15, h = lane >> 4;
-        double2 x[8];
-#pragma unroll
-        for (int c2 = 0; c2 < 8; ++c2) x[bitrev_c<3>(c2)] = tile[(2 * c2 + h) * L + v3_slot(k1, b)];
-        dit<8, -1>(x);
-        __syncwarp();
-#pragma unroll
-        for (int a2 = 0; a2 < 8; ++a2) half[i4_off(k1, h, a2)] = x[a2];
-        __syncwarp();
-        // step B, lane (g, a): S[k1][a] = (E_0 + w16^-a E_1)[k1][a mod 8] conj(tw'(k1, b + 2a)),
-        // k1 = 2k' + g; F_g = DFT-8 over k'; then the radix-2 across lanes g = 0 / 1
-        const int gp = h, aa = k1;  // lane = 16 gp + aa
-        uint32_t tw4[32];
-        tm_ld_raw<32>(tm_tw4, tw4);
-        const double2 wa = c_root64[4 * aa];  // w16^a (conjugated below)
-        double2 e[8][2];
-#pragma unroll
-        for (int k2 = 0; k2 < 8; ++k2)
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) e[k2][hh] = half[i4_off(2 * k2 + gp, hh, aa & 7)];
-        tm_wait_ld();
-#pragma unroll
-        for (int k2 = 0; k2 < 8; ++k2) {
-          const double2 t = cadd(e[k2][0], cmulc(e[k2][1], wa));
-          const uint32_t* w4 = tw4 + 4 * k2;
-          const double2 tw = make_double2(__hiloint2double(w4[1], w4[0]), __hiloint2double(w4[3], w4[2]));
-          x[bitrev_c<3>(k2)] = cmulc(t, tw);
-        }
-        dit<8, -1>(x);
-        const double sgn = gp ? -1.0 : 1.0;
-        if (active) {
-          uint32_t* Ac = acc_g + oo * N;
-#pragma unroll
-          for (int m2 = 0; m2 < 8; ++m2) {
-            const double2 mine = cmulc(x[m2], c_root64[4 * m2 * gp]);  // gp = 1: w16^-m' F_1
-            const double2 recv = shfl_xor_c(mine, 16);
-            const double2 y = make_double2(fma(sgn, mine.x, recv.x), fma(sgn, mine.y, recv.y));
-            const int m1 = m2 + 8 * gp;
-            const double2 v = cmulc(y, c_root64[G::CSTEP * m1]);  // untwist
-            const uint32_t j = (uint32_t)(L * m1 + b + 2 * aa);
-            if constexpr (PROBE) worst = fmax(worst, fmax(fabs(v.x - rint(v.x)), fabs(v.y - rint(v.y))));
-#if GW_V5_RED
-            atomicAdd(Ac + j, round_mod32(v.x));
-            atomicAdd(Ac + j + M, round_mod32(v.y));
-#else
-            Ac[j] += round_mod32(v.x);
-            Ac[j + M] += round_mod32(v.y);
-#endif
-          }
-        }
-      }
-      // ---------------- I: output oo = component oo, two warps per gate ----------------
-      const int isel = (i + gl) & 1;  // which warp pair inverts this step
-      if (!I4 && !IPAIR && (o >> 1) == isel) {
-        const int oo = o & 1;
-        double2 x[P];
-        double2* tile = U + (size_t)oo * P * L;
-#pragma unroll
-        for (int c = 0; c < P; ++c) x[bitrev_c<G::LOGP>(c)] = tile[c * L + pos];
-        fft_inverse_tail<LOGN, true>(x, tile, TwTmemHalves{tm_tw}, l);
-        if (active) {
-          uint32_t* Ac = acc_g + oo * N;
-#pragma unroll
-          for (int m1 = 0; m1 < P; ++m1) {
-            const double2 v = m1 == 0 ? x[0] : cmulc(x[m1], c_root64[G::CSTEP * m1]);
-            const uint32_t j = (uint32_t)(L * m1 + l);
-            if constexpr (PROBE) worst = fmax(worst, fmax(fabs(v.x - rint(v.x)), fabs(v.y - rint(v.y))));
-#if GW_V5_RED
-            atomicAdd(Ac + j, round_mod32(v.x));
-            atomicAdd(Ac + j + M, round_mod32(v.y));
-#else
-            Ac[j] += round_mod32(v.x);
-            Ac[j + M] += round_mod32(v.y);
-#endif
-          }
-        }
-      }
       mark(4);
-      // acc updated before the next decomposition
-      if (IPX) named_barrier(13, 128 * GC); else named_barrier(bar_id, 128);
+      named_barrier(bar_id, 128);  // acc updated before the next decomposition
       mark(5);
       slot = slot + 1 == NSLOT ? 0 : slot + 1;
     }
