@@ -219,6 +219,7 @@ def evaluate(c: Circuit, schedule: Schedule, inputs: Mapping[str, np.ndarray], k
     caller can read intermediate wires back (parity sampling); by default it
     is released when evaluate returns.
     """
+    trace = _TRACE and time.perf_counter()
     ek: EvalKey = _as_eval_key(keys)
     p = ek.params
     mats = check_inputs(c, inputs, p.n)
@@ -229,6 +230,8 @@ def evaluate(c: Circuit, schedule: Schedule, inputs: Mapping[str, np.ndarray], k
 
     plan = _cached_plan(c, schedule)
     eng = ek.engine()
+    if trace:
+        t_eng = time.perf_counter()
     metrics = Metrics(total_gates=len(c.gates), workers=schedule.workers, gpus=1)
     # The context is single-submitter: hold it for the whole evaluation so a
     # concurrent evaluate() on the same keys cannot swap the wire store under
@@ -253,6 +256,11 @@ def evaluate(c: Circuit, schedule: Schedule, inputs: Mapping[str, np.ndarray], k
             raise
         if not keep_wires:
             eng.wires_alloc(0)   # release the store (config 4: ~30 GB)
+    if trace:
+        import sys
+        t_end = time.perf_counter()
+        sys.stderr.write(f"[evaluate] keys+plan {1e3 * (t_eng - trace):.2f} ms, device run {1e3 * (t1 - t0):.2f} ms, "
+                         f"other {1e3 * (t_end - t_eng - (t1 - t0)):.2f} ms, total {1e3 * (t_end - trace):.2f} ms\n")
     per_wave = [ms / 1e3 for ms in per_wave_ms]
     start = t0
     for w, dt in enumerate(per_wave):   # spans on the monotonic clock, laid out by device time
@@ -268,6 +276,9 @@ def evaluate(c: Circuit, schedule: Schedule, inputs: Mapping[str, np.ndarray], k
     metrics.per_wave_wall_time = per_wave
     metrics.per_worker_busy_time = [metrics.device_time_seconds] + [0.0] * (schedule.workers - 1)
     return outputs, metrics
+
+
+_TRACE = bool(__import__("os").environ.get("GATEWAVE_EVAL_TRACE"))
 
 
 def _world(group):
