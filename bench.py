@@ -40,6 +40,7 @@ inputs of SURVEY.md Appendix A.  With N GPUs every rank evaluates its own
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import platform
@@ -318,7 +319,7 @@ def run_reference(args):
     return 0
 
 
-def config2_latency(ks, P, eng, repeats: int = 3):
+def config2_latency(ks, P, eng, repeats: int = 5):
     """BASELINE configs[1]: 8-bit ripple-carry adder + 8-bit multiplier,
     level-scheduled on one GPU through runtime.evaluate (host rows in, host
     rows out).  Returns app latency (median over repeats) and level shapes;
@@ -340,9 +341,14 @@ def config2_latency(ks, P, eng, repeats: int = 3):
         evaluate(c, sched, inputs, ks)  # warm
         lat, met, outs = [], None, None
         for _ in range(repeats):
-            t0 = time.perf_counter()
-            outs, met = evaluate(c, sched, inputs, ks)
-            lat.append(time.perf_counter() - t0)
+            gc.collect()          # a collection inside the timed call would be host noise, not the app
+            gc.disable()
+            try:
+                t0 = time.perf_counter()
+                outs, met = evaluate(c, sched, inputs, ks)
+                lat.append(time.perf_counter() - t0)
+            finally:
+                gc.enable()
         plain = C.simulate_plain(c, vals)
         ok = all(C.bits_to_value(decrypt_rows(ks.lwe_sk, outs[k])) == v for k, v in plain.items())
         res[name] = {"app_latency_s": statistics.median(lat), "gates": len(c.gates),
