@@ -38,14 +38,4 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     if (++spins > (1u << 24)) __trap();
   }
 }
-// Same wait for warps off the critical path (the key loaders): back off with
-// nanosleep between polls so the spin does not take issue slots from the
-// compute warps of the same sub-partition.
-__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, uint32_t ns) {
-  uint32_t spins = 0;
-  while (!mbar_try_wait(bar, parity)) {
-    if (++spins > (1u << 22)) __trap();
-    __nanosleep(ns);
-  }
-}
 }  // namespace gw
