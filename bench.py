@@ -499,6 +499,29 @@ def run_ours(args):
                 "peak_source": "measured DFMA peak, tools/microbench/pipes.cu "
                                "(profiles/r01_microbench_pipes.txt); not in MEASURED_PEAKS.json"}
 
+    # ---- informational: the same batch in exact mode (split-key v3 kernel) -----
+    exact_mode = None
+    if not args.no_netlist and not eng.exact():
+        eng.set_exact(True)
+        try:
+            for _ in range(2):
+                step()
+            torch.cuda.synchronize()
+            res_x = out[:, :W].cpu().numpy().view(np.uint32)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(5):
+                step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            xms = e0.elapsed_time(e1) / 5
+            exact_mode = {"kernel": "k_blind_rotate_v3 (16-bit split key, provably exact rounding)",
+                          "ms_per_step": xms, "gates_per_s": G / (xms / 1e3),
+                          "outputs_equal_default_kernel": bool(np.array_equal(res_x, res)),
+                          "note": "device-resident, L2 not flushed; gw_set_exact / GATEWAVE_BR_EXACT=1"}
+        finally:
+            eng.set_exact(False)
+
     # ---- informational: a wide level (12 x 148 gates, 3 per SM, 4 waves) -----
     wide = None
     if not args.no_netlist:
@@ -613,6 +636,7 @@ def run_ours(args):
             "cpu_netlists_extrapolated": cpu_c345,
             "netlists_sharded": None,
             "throughput_wide_level": wide,
+            "exact_mode": exact_mode,
             "param110": p110,
             "clocks": clk.summary(),
             "parity": parity,
