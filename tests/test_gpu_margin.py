@@ -1,13 +1,14 @@
 """Exactness margin of the FP64 external product, measured on the device.
 
-The engine computes the negacyclic products with a 16-bit-split FP64 FFT and
-rounds every inverse-transform value to the nearest integer; that recovers
-the exact integer (hence ciphertexts bit-identical to the reference's
-Goldilocks NTT) whenever |x - rint(x)| < 0.5.  The probe build of the blind
-rotation records the worst distance over every rounded value.
-Assert < 0.1 at PARAM_128 (config 1), PARAM_110, and at the engine envelope's
-edge (Bg = 10, l = 2, N = 1024: coefficients up to 2^36, where gw_set_params
-stops accepting parameter sets), bit-exact against the oracle there too."""
+The engine rounds every inverse-transform value of the blind rotation to the
+nearest integer; that recovers the exact integer (hence ciphertexts
+bit-identical to the reference's Goldilocks NTT) whenever |x - rint(x)| < 0.5.
+The probe build records the worst distance over every rounded value
+(DESIGN.md §3).  At PARAM_128 / PARAM_110 the default kernel (v5) transforms the
+full 32-bit key words (coefficients up to 2^51; measured margin ~0.03); at the
+engine envelope's edge (Bg = 10, l = 2, N = 1024), where v5 does not apply, the
+split-key kernel (v3, coefficients up to 2^36; ~7e-7) runs.  Assert < 0.1 in
+both regimes, bit-exact against the oracle / the reference's golden vectors."""
 import numpy as np
 import pytest
 
