@@ -70,11 +70,8 @@ __host__ __device__ __forceinline__ size_t v5_index(int i, int cidx, int tlane) 
 // inverting warps per gate (profiles/r02_v5_ipair_ab.txt, r02_v5_ipair_gc23_ab.txt).
 // Rejected on the same box: four warps on quarter problems with a shuffle radix-2
 // (GC = 1 5.81k), pairs across the two gates of a CTA (GC = 2 8.23k), gate stagger
-// (+1.9-2.8 %), loader nanosleep back-off (+0.7-1.7 % at GC = 2, 3).
-// GC >= 2 stagger (A/B only): gate g > 0 starts after gate 0's F(0) (1) or M(0) (2); 0 = off
-#ifndef GW_V5_STAGGER
-#define GW_V5_STAGGER 0
-#endif
+// (+1.9-2.8 % with the two-warp inverse, +0.1-1 % with pairs: profiles/r02_v5_stagger_pairs_ab.txt),
+// loader nanosleep back-off (+0.7-1.7 % at GC = 2, 3).
 #ifndef GW_V5_RED
 #define GW_V5_RED 1  // accumulator updates as shared-memory RED.ADD (same-box A/B: -0.4 / -0.7 / -1 % at GC = 1 / 2 / 3 vs load-add-store, profiles/r02_v5_stagger_red_ab.txt)
 #endif
@@ -103,8 +100,7 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
   uint64_t* bars = reinterpret_cast<uint64_t*>(xchg_all + (size_t)GC * V5::XCHG);
   uint64_t* full_bar = bars;           // [3] the loader warps stored slab i in slot i % 3
   uint64_t* empty_bar = bars + NSLOT;  // [3] every compute warp finished its MAC reads of slot i % 3
-  uint64_t* go_bar = bars + 2 * NSLOT;  // stagger (GW_V5_STAGGER)
-  uint32_t* tm_slot = reinterpret_cast<uint32_t*>(bars + 2 * NSLOT + 1);
+  uint32_t* tm_slot = reinterpret_cast<uint32_t*>(bars + 2 * NSLOT);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, l = lane;
   const int gl = warp >> 2, o = warp & 3;
@@ -133,7 +129,6 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
       mbar_init(&full_bar[k], 4);
       mbar_init(&empty_bar[k], 4 * GC);
     }
-    mbar_init(go_bar, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) tm_alloc(tm_slot, 512);
@@ -234,7 +229,6 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
     }
   } else {
     if constexpr (GC >= 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(CREG));
-    if (GW_V5_STAGGER && GC >= 2 && gl >= 1) mbar_wait(go_bar, 0);
     uint32_t a_next = lin_at(0);
     double worst = 0.0;  // PROBE only
     int slot = 0;
@@ -288,7 +282,6 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
 #pragma unroll
         for (int c = 0; c < P; ++c) tile[c * L + pos] = x[c];
       }
-      if (GW_V5_STAGGER == 1 && GC >= 2 && i == 0 && gl == 0 && lane == 0) mbar_arrive(go_bar);
       mark(0);
       named_barrier(bar_id, 128);  // U complete
       mark(1);
@@ -335,7 +328,6 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
       tm_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[slot]);
-      if (GW_V5_STAGGER == 2 && GC >= 2 && i == 0 && gl == 0 && lane == 0) mbar_arrive(go_bar);
       mark(2);
       named_barrier(bar_id, 128);  // V complete
       mark(3);
