@@ -72,6 +72,12 @@ __host__ __device__ __forceinline__ size_t v5_index(int i, int cidx, int tlane) 
 // (GC = 1 5.81k), pairs across the two gates of a CTA (GC = 2 8.23k), gate stagger
 // (+1.9-2.8 % with the two-warp inverse, +0.1-1 % with pairs: profiles/r02_v5_stagger_pairs_ab.txt),
 // loader nanosleep back-off (+0.7-1.7 % at GC = 2, 3).
+// Digit extraction with every accumulator load hoisted above the arithmetic and the
+// partner stores (bit GC-1).  Same-box A/B, cycles per step: GC = 1 5.35k -> 5.23k,
+// GC = 2 7.61k -> 7.66k (off there), GC = 3 10.07k -> 10.03k (profiles/r02_v5_digit_hoist_ab.txt)
+#ifndef GW_V5_DIGITS_HOIST
+#define GW_V5_DIGITS_HOIST 5
+#endif
 #ifndef GW_V5_RED
 #define GW_V5_RED 1  // accumulator updates as shared-memory RED.ADD (same-box A/B: -0.4 / -0.7 / -1 % at GC = 1 / 2 / 3 vs load-add-store, profiles/r02_v5_stagger_red_ab.txt)
 #endif
@@ -249,19 +255,50 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
         const uint32_t* from_partner = xg + (size_t)lv * (P / 2) * 32;
         uint32_t mine[P];
         const uint32_t idxh = idx0 + (uint32_t)(hh * M);
+        if constexpr ((GW_V5_DIGITS_HOIST >> (GC - 1)) & 1) {
+          // every accumulator read first, then the arithmetic, then the stores to the
+          // partner: a store to the exchange area may not be moved above a later load of
+          // acc by the compiler (it cannot prove the two regions disjoint), so with the
+          // loads interleaved each coefficient pair would wait for the previous pair's
+          // whole load -> digit -> store chain
+          uint32_t vrot[P], vdir[P];
 #pragma unroll
-        for (int m1 = 0; m1 < P; m1 += 2) {
-          uint32_t oth[2];
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const uint32_t idx = (idxh + (uint32_t)(L * (m1 + q))) & two_n_mask;
-            const uint32_t v = A[idx & (N - 1)];
-            const uint32_t neg = 0u - ((idx >> LOGN) & 1u);
-            const uint32_t buf = ((v ^ neg) - neg) - A[L * (m1 + q) + l + hh * M] + a.offs;
-            mine[m1 + q] = (buf >> sh_mine) & base_mask;
-            oth[q] = (buf >> sh_other) & base_mask;
+          for (int m1 = 0; m1 < P; ++m1) {
+            const uint32_t idx = (idxh + (uint32_t)(L * m1)) & two_n_mask;
+            vrot[m1] = A[idx & (N - 1)];
+            vdir[m1] = A[L * m1 + l + hh * M];
           }
-          to_partner[(m1 / 2) * 32 + lane] = oth[0] | (oth[1] << 16);
+          uint32_t packed[P / 2];
+#pragma unroll
+          for (int m1 = 0; m1 < P; m1 += 2) {
+            uint32_t oth[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const uint32_t idx = (idxh + (uint32_t)(L * (m1 + q))) & two_n_mask;
+              const uint32_t neg = 0u - ((idx >> LOGN) & 1u);
+              const uint32_t buf = ((vrot[m1 + q] ^ neg) - neg) - vdir[m1 + q] + a.offs;
+              mine[m1 + q] = (buf >> sh_mine) & base_mask;
+              oth[q] = (buf >> sh_other) & base_mask;
+            }
+            packed[m1 / 2] = oth[0] | (oth[1] << 16);
+          }
+#pragma unroll
+          for (int k = 0; k < P / 2; ++k) to_partner[k * 32 + lane] = packed[k];
+        } else {
+#pragma unroll
+          for (int m1 = 0; m1 < P; m1 += 2) {
+            uint32_t oth[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const uint32_t idx = (idxh + (uint32_t)(L * (m1 + q))) & two_n_mask;
+              const uint32_t v = A[idx & (N - 1)];
+              const uint32_t neg = 0u - ((idx >> LOGN) & 1u);
+              const uint32_t buf = ((v ^ neg) - neg) - A[L * (m1 + q) + l + hh * M] + a.offs;
+              mine[m1 + q] = (buf >> sh_mine) & base_mask;
+              oth[q] = (buf >> sh_other) & base_mask;
+            }
+            to_partner[(m1 / 2) * 32 + lane] = oth[0] | (oth[1] << 16);
+          }
         }
         named_barrier(5 + 2 * gl + cr, 64);
 #pragma unroll
