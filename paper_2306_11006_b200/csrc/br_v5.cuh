@@ -78,6 +78,12 @@ __host__ __device__ __forceinline__ size_t v5_index(int i, int cidx, int tlane) 
 #ifndef GW_V5_DIGITS_HOIST
 #define GW_V5_DIGITS_HOIST 5
 #endif
+// MAC phase with the V stores of both frequency pairs after both MACs (bit GC-1).
+// Same-box A/B, cycles per step: GC = 1 5.22k -> 5.11k; GC = 2, 3 +0.2 % (off there)
+// (profiles/r02_v5_mac_defer_ab.txt)
+#ifndef GW_V5_M_DEFER
+#define GW_V5_M_DEFER 1
+#endif
 #ifndef GW_V5_RED
 #define GW_V5_RED 1  // accumulator updates as shared-memory RED.ADD (same-box A/B: -0.4 / -0.7 / -1 % at GC = 1 / 2 / 3 vs load-add-store, profiles/r02_v5_stagger_red_ab.txt)
 #endif
@@ -326,6 +332,10 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
       mbar_wait(&full_bar[slot], (uint32_t)((i / NSLOT) & 1));
       tm_fence_after();
       const uint32_t tm_slab = tm_warp + (uint32_t)(slot * COLS);
+      // GW_V5_M_DEFER: the V stores of both pairs after both MACs, so pair 1's loads need
+      // not wait for pair 0's stores (the compiler keeps stores and later loads of U in order)
+      constexpr bool kDefer = (GW_V5_M_DEFER >> (GC - 1)) & 1;
+      double2 vout[2][2][2];  // [p][output][b], kDefer only
 #pragma unroll
       for (int p = 0; p < 2; ++p) {
         const int c = mc0 + p;
@@ -357,10 +367,27 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
             }
 #pragma unroll
         for (int oo = 0; oo < 2; ++oo) {
-          double2* row = U + ((size_t)oo * P + c) * L;
-          row[v3_slot(mk1, 0)] = cadd(O[oo][0], O[oo][1]);
-          row[v3_slot(mk1, 1)] = cmulc(csub(O[oo][0], O[oo][1]), tw);
+          const double2 v0 = cadd(O[oo][0], O[oo][1]);
+          const double2 v1 = cmulc(csub(O[oo][0], O[oo][1]), tw);
+          if constexpr (kDefer) {
+            vout[p][oo][0] = v0;
+            vout[p][oo][1] = v1;
+          } else {
+            double2* row = U + ((size_t)oo * P + c) * L;
+            row[v3_slot(mk1, 0)] = v0;
+            row[v3_slot(mk1, 1)] = v1;
+          }
         }
+      }
+      if constexpr (kDefer) {
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+          for (int oo = 0; oo < 2; ++oo) {
+            double2* row = U + ((size_t)oo * P + mc0 + p) * L;
+            row[v3_slot(mk1, 0)] = vout[p][oo][0];
+            row[v3_slot(mk1, 1)] = vout[p][oo][1];
+          }
       }
       tm_fence_before();
       __syncwarp();
