@@ -81,6 +81,12 @@ __host__ __device__ __forceinline__ size_t v5_index(int i, int cidx, int tlane) 
 // MAC phase with the V stores of both frequency pairs after both MACs (bit GC-1).
 // Same-box A/B, cycles per step: GC = 1 5.22k -> 5.11k; GC = 2, 3 +0.2 % (off there)
 // (profiles/r02_v5_mac_defer_ab.txt)
+// B3 as a barrier of the inverting pair only (bit GC-1), with V_1 in U row 2 and each
+// pair's scratch in its own odd row.  Same-box A/B, cycles per step: GC = 1 5.12k -> 5.03k,
+// GC = 2 7.72k -> 7.59k, GC = 3 10.02k -> 9.93k (profiles/r02_v5_pair_b3_ab.txt)
+#ifndef GW_V5_PAIR_B3
+#define GW_V5_PAIR_B3 7
+#endif
 #ifndef GW_V5_M_DEFER
 #define GW_V5_M_DEFER 1
 #endif
@@ -193,6 +199,13 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
 
   const int mk1 = lane & 15;
   const int mc0 = 4 * o + 2 * (lane >> 4);
+  // U row that receives V_oo (the MAC output of accumulator component oo)
+  constexpr bool kPairB3 = (GW_V5_PAIR_B3 >> (GC - 1)) & 1;
+  auto v_row = [](int oo) { return kPairB3 ? 2 * oo : oo; };
+  // the paired inverse's named barrier: warps (2 oo, 2 oo + 1) of gate gl
+  // (ids: 1..GC per gate for B1-B3, 5..4+2GC the F level pairs)
+  const int kPairQ = 2 * gl + (o >> 1);
+  const int kPairBar = GC == 3 ? (kPairQ == 0 ? 4 : 10 + kPairQ) : 9 + kPairQ;
   const int pos = v3_pos(l);
   const int bar_id = 1 + gl;
 
@@ -373,7 +386,7 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
             vout[p][oo][0] = v0;
             vout[p][oo][1] = v1;
           } else {
-            double2* row = U + ((size_t)oo * P + c) * L;
+            double2* row = U + ((size_t)v_row(oo) * P + c) * L;
             row[v3_slot(mk1, 0)] = v0;
             row[v3_slot(mk1, 1)] = v1;
           }
@@ -384,7 +397,7 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
         for (int p = 0; p < 2; ++p)
 #pragma unroll
           for (int oo = 0; oo < 2; ++oo) {
-            double2* row = U + ((size_t)oo * P + mc0 + p) * L;
+            double2* row = U + ((size_t)v_row(oo) * P + mc0 + p) * L;
             row[v3_slot(mk1, 0)] = vout[p][oo][0];
             row[v3_slot(mk1, 1)] = vout[p][oo][1];
           }
@@ -399,11 +412,11 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
       {
         // warps (2 oo, 2 oo + 1) invert component oo; role rr: even (0) / odd (1) outputs
         const int rr = o & 1, oo = o >> 1;
-        // named barrier ids: 1..GC per gate (B1-B3), 5..4+2GC the F level pairs
-        const int pq = 2 * gl + oo;
-        const int pair_bar = GC == 3 ? (pq == 0 ? 4 : 10 + pq) : 9 + pq;
-        const double2* tileV = U + (size_t)oo * P * L;
-        double2* scratch = U + (size_t)(2 + oo) * P * L;   // rows 2, 3 are free after M
+        const int pair_bar = kPairBar;
+        const double2* tileV = U + (size_t)v_row(oo) * P * L;
+        // the scratch row is free after M: rows 2, 3 (V in rows 0, 1), or row 2 oo + 1 when
+        // V_oo sits in row 2 oo (GW_V5_PAIR_B3: each pair then touches only its own rows)
+        double2* scratch = U + (size_t)(kPairB3 ? 2 * oo + 1 : 2 + oo) * P * L;
         uint32_t tw8[32];
         tm_ld_raw<32>(tm_tw4 + (uint32_t)(32 * rr), tw8);
         // pass 1, lane (k1, b): T[2a' + rr] = DFT-8_{c'} of (V[c'] +- V[c'+8]) w16^(-rr c')
@@ -459,7 +472,10 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
         }
       }
       mark(4);
-      named_barrier(bar_id, 128);  // acc updated before the next decomposition
+      // acc updated before the next decomposition.  With GW_V5_PAIR_B3 only the pair that
+      // updated component oo waits: the same two warps decompose component oo next, read
+      // only acc[oo], and write only U rows 2 oo, 2 oo + 1, which no other warp reads before B1.
+      if constexpr (kPairB3) named_barrier(kPairBar, 64); else named_barrier(bar_id, 128);
       mark(5);
       slot = slot + 1 == NSLOT ? 0 : slot + 1;
     }
@@ -470,9 +486,12 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
     }
     if (prof)
       for (int ph = 0; ph < 6; ++ph) a.prof[o * 6 + ph] = pt_[ph];
-    if (active && o < 2) {
-      uint32_t* dst = a.acc_out + ((size_t)g * 2 + o) * N;
-      for (int j = lane; j < N; j += 32) dst[j] = acc_g[o * N + j];
+    // component c is written back by warp 2c, one of the two warps that updated it (the
+    // pair's last barrier orders their updates; with GW_V5_PAIR_B3 nothing else does)
+    if (active && (o & 1) == 0) {
+      const int cc = o >> 1;
+      uint32_t* dst = a.acc_out + ((size_t)g * 2 + cc) * N;
+      for (int j = lane; j < N; j += 32) dst[j] = acc_g[cc * N + j];
     }
   }
   tm_fence_before();
