@@ -339,7 +339,7 @@ def config2_latency(ks, P, eng, repeats: int = 5):
                   for p in c.inputs}
         sched = build_schedule(c, 1)
         evaluate(c, sched, inputs, ks)  # warm
-        lat, met, outs = [], None, None
+        lat, met, outs, phases = [], None, None, []
         for _ in range(repeats):
             gc.collect()          # a collection inside the timed call would be host noise, not the app
             gc.disable()
@@ -349,12 +349,13 @@ def config2_latency(ks, P, eng, repeats: int = 5):
                 lat.append(time.perf_counter() - t0)
             finally:
                 gc.enable()
+            phases.append({k: round(v, 6) for k, v in met.host_phases.items()})
         plain = C.simulate_plain(c, vals)
         ok = all(C.bits_to_value(decrypt_rows(ks.lwe_sk, outs[k])) == v for k, v in plain.items())
         res[name] = {"app_latency_s": statistics.median(lat), "gates": len(c.gates),
                      "bootstraps": met.bootstrap_count, "levels": len(sched.waves),
                      "device_time_s": met.device_time_seconds, "wall_runs_s": lat,
-                     "evaluate_wall_s": met.wall_time_seconds, "decrypt_ok": ok}
+                     "evaluate_wall_s": met.wall_time_seconds, "host_phases_s": phases, "decrypt_ok": ok}
     res["total_app_latency_s"] = sum(v["app_latency_s"] for v in res.values())
     return res
 

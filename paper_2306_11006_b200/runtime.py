@@ -54,6 +54,10 @@ class Metrics:
     spans: list[tuple[int, int, float, float]] = field(default_factory=list)
     device_time_seconds: float = 0.0
     gpus: int = 1
+    # host-side phases of this evaluate() call in seconds (not part of the reference's JSON):
+    # keys (eval key + engine lookup), wires (store allocation + input upload), plan, run
+    # (all levels, one sync), outputs (download + store release)
+    host_phases: dict = field(default_factory=dict)
 
     def as_dict(self) -> dict:
         return {
@@ -219,7 +223,7 @@ def evaluate(c: Circuit, schedule: Schedule, inputs: Mapping[str, np.ndarray], k
     caller can read intermediate wires back (parity sampling); by default it
     is released when evaluate returns.
     """
-    trace = _TRACE and time.perf_counter()
+    t_start = time.perf_counter()
     ek: EvalKey = _as_eval_key(keys)
     p = ek.params
     mats = check_inputs(c, inputs, p.n)
@@ -230,8 +234,7 @@ def evaluate(c: Circuit, schedule: Schedule, inputs: Mapping[str, np.ndarray], k
 
     plan = _cached_plan(c, schedule)
     eng = ek.engine()
-    if trace:
-        t_eng = time.perf_counter()
+    t_keys = time.perf_counter()
     metrics = Metrics(total_gates=len(c.gates), workers=schedule.workers, gpus=1)
     # The context is single-submitter: hold it for the whole evaluation so a
     # concurrent evaluate() on the same keys cannot swap the wire store under
@@ -241,7 +244,9 @@ def evaluate(c: Circuit, schedule: Schedule, inputs: Mapping[str, np.ndarray], k
         try:
             for port in c.inputs:
                 eng.wires_put(np.asarray(port.wires, np.int64), mats[port.name])
+            t_wires = time.perf_counter()
             handle = eng.plan_create(plan.level_offsets, plan.opcodes, plan.operands, plan.out_ids)
+            t_plan = time.perf_counter()
             try:
                 # every level enqueued back to back on the engine stream, an event
                 # mark at each level boundary, ONE host synchronisation at the end
@@ -256,11 +261,9 @@ def evaluate(c: Circuit, schedule: Schedule, inputs: Mapping[str, np.ndarray], k
             raise
         if not keep_wires:
             eng.wires_alloc(0)   # release the store (config 4: ~30 GB)
-    if trace:
-        import sys
-        t_end = time.perf_counter()
-        sys.stderr.write(f"[evaluate] keys+plan {1e3 * (t_eng - trace):.2f} ms, device run {1e3 * (t1 - t0):.2f} ms, "
-                         f"other {1e3 * (t_end - t_eng - (t1 - t0)):.2f} ms, total {1e3 * (t_end - trace):.2f} ms\n")
+    t_end = time.perf_counter()
+    metrics.host_phases = {"keys": t_keys - t_start, "wires": t_wires - t_keys, "plan": t_plan - t_wires,
+                           "run": t1 - t0, "outputs": t_end - t_plan - (t1 - t0)}
     per_wave = [ms / 1e3 for ms in per_wave_ms]
     start = t0
     for w, dt in enumerate(per_wave):   # spans on the monotonic clock, laid out by device time
@@ -276,9 +279,6 @@ def evaluate(c: Circuit, schedule: Schedule, inputs: Mapping[str, np.ndarray], k
     metrics.per_wave_wall_time = per_wave
     metrics.per_worker_busy_time = [metrics.device_time_seconds] + [0.0] * (schedule.workers - 1)
     return outputs, metrics
-
-
-_TRACE = bool(__import__("os").environ.get("GATEWAVE_EVAL_TRACE"))
 
 
 def _world(group):
