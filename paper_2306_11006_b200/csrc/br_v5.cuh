@@ -90,10 +90,6 @@ __host__ __device__ __forceinline__ size_t v5_index(int i, int cidx, int tlane) 
 #ifndef GW_V5_M_DEFER
 #define GW_V5_M_DEFER 1
 #endif
-// Forward lane twiddles double-buffered from TMEM (bit GC-1)
-#ifndef GW_V5_TWPIPE
-#define GW_V5_TWPIPE 0
-#endif
 #ifndef GW_V5_RED
 #define GW_V5_RED 1  // accumulator updates as shared-memory RED.ADD (same-box A/B: -0.4 / -0.7 / -1 % at GC = 1 / 2 / 3 vs load-add-store, profiles/r02_v5_stagger_red_ab.txt)
 #endif
@@ -104,37 +100,6 @@ __host__ __device__ __forceinline__ size_t v5_index(int i, int cidx, int tlane) 
 #ifndef GW_V5_LREG3
 #define GW_V5_LREG3 56
 #endif
-
-// Forward head (fft.cuh fft_forward_head) with the lane twiddles streamed from TMEM
-// four at a time and double-buffered: chunk 0 is requested before the first DFT-16,
-// chunk q + 1 while chunk q is multiplied, so no TMEM load latency is exposed.
-__device__ __forceinline__ void v5_forward_head_pipelined(double2 (&x)[V5::P], double2* tile, uint32_t tm_tw, int l) {
-  constexpr int P = V5::P, L = V5::L, LOGP = V5::G::LOGP;
-  uint32_t tb[2][16];
-  tm_ld_raw<16>(tm_tw, tb[0]);
-  dit<P, +1>(x);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    tm_wait_ld();
-    if (q + 1 < 4) tm_ld_raw<16>(tm_tw + (uint32_t)(16 * (q + 1)), tb[(q + 1) & 1]);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t* w = tb[q & 1] + 4 * k;
-      x[4 * q + k] = cmul(x[4 * q + k], make_double2(__hiloint2double(w[1], w[0]), __hiloint2double(w[3], w[2])));
-    }
-  }
-  __syncwarp();
-#pragma unroll
-  for (int k1 = 0; k1 < P; ++k1) tile[k1 * L + swz(k1, l)] = x[k1];
-  __syncwarp();
-  {
-    const int k1 = l >> 1, b = l & 1;
-#pragma unroll
-    for (int a = 0; a < P; ++a) x[bitrev_c<LOGP>(a)] = tile[k1 * L + swz(k1, b + 2 * a)];
-  }
-  __syncwarp();
-  dit<P, +1>(x);  // x[c] = u_b[c]
-}
 
 template <int GC, bool PROBE = false>
 __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a) {
@@ -368,11 +333,7 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
           }
         }
         double2* tile = U + (size_t)o * P * L;
-        if constexpr ((GW_V5_TWPIPE >> (GC - 1)) & 1) {
-          v5_forward_head_pipelined(x, tile, tm_tw, l);
-        } else {
-          fft_forward_head<LOGN, true>(x, tile, TwTmemHalves{tm_tw}, l);
-        }
+        fft_forward_head<LOGN, true>(x, tile, TwTmemHalves{tm_tw}, l);
         __syncwarp();
 #pragma unroll
         for (int c = 0; c < P; ++c) tile[c * L + pos] = x[c];
