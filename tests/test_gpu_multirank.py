@@ -64,9 +64,14 @@ def test_two_ranks_one_gpu_match_single_process():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    got = dict(q.get(timeout=300) for _ in procs)
-    for p in procs:
-        p.join(timeout=60)
+    try:
+        got = dict(q.get(timeout=300) for _ in procs)
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():  # never leave a rank behind to disturb later runs on this box
+                p.kill()
+                p.join()
     want = _single()
     assert got[0] == want and got[1] == want
 
@@ -115,12 +120,17 @@ def test_two_gpus_native_nccl_exchange_matches_single_process():
     for p in procs:
         p.start()
     got = {}
-    for _ in procs:
-        rank, res, tr = q.get(timeout=300)
-        got[rank] = res
-        assert tr == ["nccl"] * 3
-    for p in procs:
-        p.join(timeout=60)
+    try:
+        for _ in procs:
+            rank, res, tr = q.get(timeout=300)
+            got[rank] = res
+            assert tr == ["nccl"] * 3
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():  # never leave a rank behind to disturb later runs on this box
+                p.kill()
+                p.join()
     want = _single()
     assert got[0] == want and got[1] == want
 

@@ -83,9 +83,14 @@ def test_multi_rank_exchange_matches_plaintext(world):
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = dict(q.get(timeout=180) for _ in procs)
-    for p in procs:
-        p.join(timeout=60)
+    try:
+        res = dict(q.get(timeout=180) for _ in procs)
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():  # never leave a rank behind to disturb later runs on this box
+                p.kill()
+                p.join()
     for rank in range(world):
         for ok, gpus, _ in res[rank]:
             assert ok and gpus == world
