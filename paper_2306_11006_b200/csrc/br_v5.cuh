@@ -90,6 +90,15 @@ __host__ __device__ __forceinline__ size_t v5_index(int i, int cidx, int tlane) 
 #ifndef GW_V5_M_DEFER
 #define GW_V5_M_DEFER 1
 #endif
+// MAC lanes own the frequency pair (c', c' + 8) (c' = 2w + lane / 16) instead of (c, c + 1),
+// so the MAC phase can hand the paired inverse its DIF-split inputs directly:
+// V[c'] + V[c' + 8] in slot c' and (V[c'] - V[c' + 8]) w16^(-c') in slot c' + 8, and each
+// inverting warp reads 8 values instead of 16.  Global (it changes the key image layout).
+// Same-box A/B, cycles per step: GC = 1 5.17k -> 4.97k, GC = 2 7.63k -> 7.40k,
+// GC = 3 10.01k -> 9.78k (profiles/r02_v5_msplit_ab.txt)
+#ifndef GW_V5_MSPLIT
+#define GW_V5_MSPLIT 1
+#endif
 #ifndef GW_V5_RED
 #define GW_V5_RED 1  // accumulator updates as shared-memory RED.ADD (same-box A/B: -0.4 / -0.7 / -1 % at GC = 1 / 2 / 3 vs load-add-store, profiles/r02_v5_stagger_red_ab.txt)
 #endif
@@ -199,6 +208,8 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
 
   const int mk1 = lane & 15;
   const int mc0 = 4 * o + 2 * (lane >> 4);
+  // MAC-phase frequency of pair p owned by this lane (see GW_V5_MSPLIT)
+  auto mfreq = [&](int p) { return GW_V5_MSPLIT ? 2 * o + (lane >> 4) + 8 * p : mc0 + p; };
   // U row that receives V_oo (the MAC output of accumulator component oo)
   constexpr bool kPairB3 = (GW_V5_PAIR_B3 >> (GC - 1)) & 1;
   auto v_row = [](int oo) { return kPairB3 ? 2 * oo : oo; };
@@ -347,11 +358,11 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
       const uint32_t tm_slab = tm_warp + (uint32_t)(slot * COLS);
       // GW_V5_M_DEFER: the V stores of both pairs after both MACs, so pair 1's loads need
       // not wait for pair 0's stores (the compiler keeps stores and later loads of U in order)
-      constexpr bool kDefer = (GW_V5_M_DEFER >> (GC - 1)) & 1;
+      constexpr bool kDefer = GW_V5_MSPLIT || ((GW_V5_M_DEFER >> (GC - 1)) & 1);
       double2 vout[2][2][2];  // [p][output][b], kDefer only
 #pragma unroll
       for (int p = 0; p < 2; ++p) {
-        const int c = mc0 + p;
+        const int c = mfreq(p);
         const double2 tw = c_root64[2 * c];  // e^{2 pi i c / 32}
         uint32_t kw[2][32];
         // both s halves of this pair's keys: 2 x 32 columns (8 complex each)
@@ -392,7 +403,21 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
           }
         }
       }
-      if constexpr (kDefer) {
+      if constexpr (GW_V5_MSPLIT) {
+        // the paired inverse's DIF split of pass 1, done here: slot c' <- V[c'] + V[c'+8],
+        // slot c'+8 <- (V[c'] - V[c'+8]) w16^(-c')
+        const int c1 = mfreq(0);
+#pragma unroll
+        for (int oo = 0; oo < 2; ++oo)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            const double2 dsum = cadd(vout[0][oo][b], vout[1][oo][b]);
+            double2 ddif = csub(vout[0][oo][b], vout[1][oo][b]);
+            if (c1 != 0) ddif = cmulc(ddif, c_root64[4 * c1]);
+            U[((size_t)v_row(oo) * P + c1) * L + v3_slot(mk1, b)] = dsum;
+            U[((size_t)v_row(oo) * P + c1 + 8) * L + v3_slot(mk1, b)] = ddif;
+          }
+      } else if constexpr (kDefer) {
 #pragma unroll
         for (int p = 0; p < 2; ++p)
 #pragma unroll
@@ -421,7 +446,10 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
         tm_ld_raw<32>(tm_tw4 + (uint32_t)(32 * rr), tw8);
         // pass 1, lane (k1, b): T[2a' + rr] = DFT-8_{c'} of (V[c'] +- V[c'+8]) w16^(-rr c')
         double2 x[8];
-        {
+        if constexpr (GW_V5_MSPLIT) {  // the MAC phase wrote this role's DIF-split inputs
+#pragma unroll
+          for (int c2 = 0; c2 < 8; ++c2) x[bitrev_c<3>(c2)] = tileV[(8 * rr + c2) * L + pos];
+        } else {
           double2 v[16];
 #pragma unroll
           for (int c = 0; c < P; ++c) v[c] = tileV[c * L + pos];
@@ -537,7 +565,7 @@ __global__ void __launch_bounds__(128) k_bk_to_v5(const uint32_t* __restrict__ b
   for (int w = 0; w < 4; ++w)
 #pragma unroll
     for (int p = 0; p < 2; ++p) {
-      const int cf = 4 * w + 2 * (lane >> 4) + p;
+      const int cf = GW_V5_MSPLIT ? 2 * w + (lane >> 4) + 8 * p : 4 * w + 2 * (lane >> 4) + p;
       const double2 u0 = tile[cf * L + v3_slot(k1, 0)], u1 = tile[cf * L + v3_slot(k1, 1)];
       const double2 t = cmul(u1, c_root64[2 * cf]);
 #pragma unroll
