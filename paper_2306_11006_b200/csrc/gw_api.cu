@@ -80,7 +80,8 @@ struct gw_ctx {
   cudaEvent_t desc_copied = nullptr;  // the last H2D copy out of desc_host
   // wire store
   uint32_t* wires = nullptr;
-  int64_t wire_slots = 0;
+  int64_t wire_slots = 0;    // slots in use (0: no store)
+  int64_t wires_cap = 0;     // slots allocated (owned stores are reused while they fit)
   bool wires_owned = true;   // false when attached to caller memory (torch)
   // device descriptors of homogeneous gate batches, keyed by (opcode, B)
   std::map<uint64_t, BatchDesc> batch_desc;
@@ -1229,19 +1230,35 @@ int gw_eval_gate_batch(gw_ctx* c, int opcode, const uint32_t* const* ops, int ar
   return GW_OK;
 }
 
+// Owned wire stores are cached: a request that fits the allocated capacity reuses it, and
+// releasing (slots = 0) keeps stores up to kWireKeepBytes.  cudaMalloc / cudaFree
+// synchronise the device and were measured taking up to 0.8 s right after another
+// process released GPU memory; a netlist evaluation allocates and releases its store
+// every call (runtime.evaluate), so small stores must not go back to the driver.
+constexpr size_t kWireKeepBytes = (size_t)256 << 20;
+
 int gw_wires_alloc(gw_ctx* c, int64_t slots) {
   if (!c || slots < 0) return GW_ERR_ARG;
   if (!c->have_params) return fail(c, GW_ERR_STATE, "parameters not set");
   cudaSetDevice(c->device);
+  const size_t row_bytes = (size_t)c->Wp * sizeof(uint32_t);
+  if (c->wires_owned && c->wires && slots <= c->wires_cap &&
+      (slots > 0 || (size_t)c->wires_cap * row_bytes <= kWireKeepBytes)) {
+    c->wire_slots = slots;  // stream-ordered reuse: earlier work on the store precedes the memset
+    if (slots) GW_CUDA(c, cudaMemsetAsync(c->wires, 0, (size_t)slots * row_bytes, c->stream));
+    return GW_OK;
+  }
   GW_CUDA(c, cudaStreamSynchronize(c->stream));
   if (c->wires_owned) cudaFree(c->wires);
   c->wires = nullptr;
   c->wire_slots = 0;
+  c->wires_cap = 0;
   c->wires_owned = true;
   if (slots == 0) return GW_OK;
-  GW_CUDA(c, cudaMalloc(&c->wires, (size_t)slots * c->Wp * sizeof(uint32_t)));
-  GW_CUDA(c, cudaMemsetAsync(c->wires, 0, (size_t)slots * c->Wp * sizeof(uint32_t), c->stream));
+  GW_CUDA(c, cudaMalloc(&c->wires, (size_t)slots * row_bytes));
+  GW_CUDA(c, cudaMemsetAsync(c->wires, 0, (size_t)slots * row_bytes, c->stream));
   c->wire_slots = slots;
+  c->wires_cap = slots;
   return GW_OK;
 }
 
@@ -1254,13 +1271,14 @@ int gw_wires_attach(gw_ctx* c, void* dev_ptr, int64_t slots, int64_t stride_word
   if (c->wires_owned) cudaFree(c->wires);
   c->wires = (uint32_t*)dev_ptr;
   c->wire_slots = slots;
+  c->wires_cap = 0;
   c->wires_owned = false;
   return GW_OK;
 }
 
 int gw_wires_device_ptr(gw_ctx* c, void** ptr, int64_t* stride) {
   if (!c || !ptr || !stride) return GW_ERR_ARG;
-  *ptr = c->wires;
+  *ptr = c->wire_slots ? c->wires : nullptr;  // a released (cached) store is not handed out
   *stride = c->Wp;
   return GW_OK;
 }
@@ -1273,7 +1291,7 @@ static int check_ids(gw_ctx* c, const int64_t* ids, int64_t count) {
 
 int gw_wires_put(gw_ctx* c, const int64_t* ids, const uint32_t* rows, int64_t count) {
   if (!c || count < 0 || (count > 0 && (!ids || !rows))) return GW_ERR_ARG;
-  if (!c->wires) return fail(c, GW_ERR_STATE, "wire store not allocated");
+  if (!c->wires || c->wire_slots == 0) return fail(c, GW_ERR_STATE, "wire store not allocated");
   int rc = check_ids(c, ids, count);
   if (rc) return rc;
   if (count == 0) return GW_OK;
@@ -1294,7 +1312,7 @@ int gw_wires_put(gw_ctx* c, const int64_t* ids, const uint32_t* rows, int64_t co
 
 int gw_wires_get(gw_ctx* c, const int64_t* ids, uint32_t* rows, int64_t count) {
   if (!c || count < 0 || (count > 0 && (!ids || !rows))) return GW_ERR_ARG;
-  if (!c->wires) return fail(c, GW_ERR_STATE, "wire store not allocated");
+  if (!c->wires || c->wire_slots == 0) return fail(c, GW_ERR_STATE, "wire store not allocated");
   int rc = check_ids(c, ids, count);
   if (rc) return rc;
   if (count == 0) return GW_OK;
@@ -1391,7 +1409,7 @@ int gw_plan_run_levels(gw_ctx* c, gw_plan* p, int64_t first, int64_t last) {
   int rc = ready(c);
   if (rc) return rc;
   if (!p) return fail(c, GW_ERR_ARG, "null plan");
-  if (!c->wires) return fail(c, GW_ERR_STATE, "wire store not allocated");
+  if (!c->wires || c->wire_slots == 0) return fail(c, GW_ERR_STATE, "wire store not allocated");
   // the store may have been re-allocated (smaller) since the plan was built
   if (p->max_wire >= c->wire_slots)
     return fail(c, GW_ERR_WIRE, "plan references wire " + std::to_string(p->max_wire) + " but the wire store has " +
@@ -1528,7 +1546,7 @@ int gw_xplan_buffers(gw_ctx* c, const gw_xplan* x, void** d_send, void** d_recv)
 
 int gw_exchange_pack(gw_ctx* c, const gw_xplan* x, int64_t level, uint32_t* d_send) {
   if (!c || !x || level < 0 || level >= x->n_levels) return GW_ERR_ARG;
-  if (!c->wires) return fail(c, GW_ERR_STATE, "wire store not allocated");
+  if (!c->wires || c->wire_slots == 0) return fail(c, GW_ERR_STATE, "wire store not allocated");
   const int64_t n = x->send_tot[level];
   if (n == 0) return GW_OK;
   if (!d_send) d_send = x->d_send;
@@ -1541,7 +1559,7 @@ int gw_exchange_pack(gw_ctx* c, const gw_xplan* x, int64_t level, uint32_t* d_se
 
 int gw_exchange_unpack(gw_ctx* c, const gw_xplan* x, int64_t level, const uint32_t* d_recv) {
   if (!c || !x || level < 0 || level >= x->n_levels) return GW_ERR_ARG;
-  if (!c->wires) return fail(c, GW_ERR_STATE, "wire store not allocated");
+  if (!c->wires || c->wire_slots == 0) return fail(c, GW_ERR_STATE, "wire store not allocated");
   const int64_t n = x->recv_tot[level];
   if (n == 0) return GW_OK;
   if (!d_recv) d_recv = x->d_recv;
