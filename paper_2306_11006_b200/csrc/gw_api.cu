@@ -1231,11 +1231,12 @@ int gw_eval_gate_batch(gw_ctx* c, int opcode, const uint32_t* const* ops, int ar
 }
 
 // Owned wire stores are cached: a request that fits the allocated capacity reuses it, and
-// releasing (slots = 0) keeps stores up to kWireKeepBytes.  cudaMalloc / cudaFree
+// releasing (slots = 0) keeps stores up to kWireKeepBytes (4 GB of the 180 GB: configs 2, 3
+// and 5 stay resident; config 4's 30 GB store goes back to the driver).  cudaMalloc / cudaFree
 // synchronise the device and were measured taking up to 0.8 s right after another
 // process released GPU memory; a netlist evaluation allocates and releases its store
 // every call (runtime.evaluate), so small stores must not go back to the driver.
-constexpr size_t kWireKeepBytes = (size_t)256 << 20;
+constexpr size_t kWireKeepBytes = (size_t)4 << 30;
 
 int gw_wires_alloc(gw_ctx* c, int64_t slots) {
   if (!c || slots < 0) return GW_ERR_ARG;
