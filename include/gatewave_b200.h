@@ -109,7 +109,11 @@ int gw_eval_gate_batch_device(gw_ctx* ctx, int opcode, const uint32_t* const* d_
  * device-resident wire store of `slots` rows and a level plan.  A plan holds,
  * per level, every gate's opcode, up to three operand wire ids (unused = -1)
  * and output wire id; gw_plan_run enqueues all levels on the stream without
- * host synchronisation (one fused launch set per level, all opcodes mixed). */
+ * host synchronisation (one fused launch set per level, all opcodes mixed).
+ * gw_wires_alloc(ctx, slots) (re)sizes the store and zeroes the slots in use;
+ * slots = 0 releases it.  An owned store is reused while it fits, and a released
+ * store of up to 4 GB stays cached for the next call (cudaMalloc / cudaFree
+ * synchronise the device); after release the store counts as absent. */
 int gw_wires_alloc(gw_ctx* ctx, int64_t slots);
 int gw_wires_put(gw_ctx* ctx, const int64_t* ids, const uint32_t* rows, int64_t count);
 int gw_wires_get(gw_ctx* ctx, const int64_t* ids, uint32_t* rows, int64_t count);
