@@ -119,6 +119,7 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
   using G = V5::G;
   constexpr int N = V5::N, M = V5::M, P = V5::P, L = V5::L, R = V5::R, LEV = V5::LEV, LOGN = V5::LOGN;
   constexpr int UB = V5::UB, COLS = V5::COLS, CIDX = V5::CIDX, NSLOT = V5::NSLOT;
+  constexpr int TWCOL = V5::TWCOL, TW4COL = V5::TW4COL;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   double2* ubuf_all = reinterpret_cast<double2*>(smem_raw);  // GC x [row][c][pos]
@@ -164,8 +165,8 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
   tm_fence_after();
   const uint32_t tm_base = *tm_slot;
   const uint32_t tm_warp = tm_base + ((uint32_t)(32 * o) << 16);
-  const uint32_t tm_tw = tm_warp + (uint32_t)V5::TWCOL;
-  const uint32_t tm_tw4 = tm_warp + (uint32_t)V5::TW4COL;
+  const uint32_t tm_tw = tm_warp + (uint32_t)TWCOL;
+  const uint32_t tm_tw4 = tm_warp + (uint32_t)TW4COL;
   if (gl == 0 && warp < 4 * GC) {
 #pragma unroll
     for (int k1 = 0; k1 < P; ++k1) tm_st4(tm_tw + (uint32_t)(4 * k1), __ldg(a.tables + 2 * G::TILE + k1 * L + l));

@@ -53,6 +53,20 @@ __global__ void k_bw(uint32_t* out, long long* cyc) {
         const uint4 v = p[((i + k + warp) & 15) * 32];
         acc += v.x ^ v.y ^ v.z ^ v.w;
       }
+    } else if constexpr (MODE == 3) {
+      if (warp & 1) {
+        const uint4* p = sm + lane;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint4 v = p[((i + k + warp) & 15) * 32];
+          acc += v.x ^ v.y ^ v.z ^ v.w;
+        }
+      } else {
+        uint32_t v = acc + i;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) v += __shfl_xor_sync(0xffffffffu, v, (k & 15) + 1);
+        acc += v;
+      }
     } else {
       uint32_t v = acc + i;
 #pragma unroll
@@ -92,5 +106,6 @@ int main() {
   for (int w : {4, 8, 16}) run<0>("tmem", w);
   for (int w : {4, 8, 16}) run<1>("smem", w);
   for (int w : {4, 8, 16}) run<2>("shfl", w);
+  for (int w : {8, 16}) run<3>("mixed", w);
   return 0;
 }
