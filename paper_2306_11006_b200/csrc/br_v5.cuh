@@ -99,6 +99,13 @@ __host__ __device__ __forceinline__ size_t v5_index(int i, int cidx, int tlane) 
 #ifndef GW_V5_MSPLIT
 #define GW_V5_MSPLIT 1
 #endif
+// L2 bulk prefetch of the key slab GW_V5_L2PF steps ahead (v3 uses 2).  With v5's 64 KB
+// slabs it does not pay: same-box A/B, distance 0 vs 2: -0.8 / -0.4 / -0.3 % per step at
+// GC = 1 / 2 / 3 with the key L2-resident, +0.2 % bench value with L2 flushed between steps
+// (profiles/r02_v5_l2pf_ab.txt)
+#ifndef GW_V5_L2PF
+#define GW_V5_L2PF 0
+#endif
 #ifndef GW_V5_RED
 #define GW_V5_RED 1  // accumulator updates as shared-memory RED.ADD (same-box A/B: -0.4 / -0.7 / -1 % at GC = 1 / 2 / 3 vs load-add-store, profiles/r02_v5_stagger_red_ab.txt)
 #endif
@@ -239,9 +246,9 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
     int slot = 0;
     for (int i = 0; i < a.n; ++i) {
       const double2* src = src_w + (size_t)i * CIDX * 128;
-#if GW_L2PF
-      if (o == 0 && lane == 0 && i + GW_L2PF < a.n) {
-        const char* pf = reinterpret_cast<const char*>(a.bk + (size_t)(i + GW_L2PF) * CIDX * 128);
+#if GW_V5_L2PF
+      if (o == 0 && lane == 0 && i + GW_V5_L2PF < a.n) {
+        const char* pf = reinterpret_cast<const char*>(a.bk + (size_t)(i + GW_V5_L2PF) * CIDX * 128);
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf), "r"(V5::SLAB) : "memory");
       }
 #endif
