@@ -61,48 +61,47 @@ __host__ __device__ __forceinline__ size_t v5_index(int i, int cidx, int tlane) 
   return ((size_t)i * V5::CIDX + cidx) * 128 + tlane;
 }
 
-// Paired split inverse: two warps of a gate invert one accumulator component together,
-// each doing the odd or even outputs of both DFT-16 passes (decimation in frequency:
-// both read all 16 inputs, form the 8 half-sums or twisted half-differences and run a
-// DFT-8), with the lane twiddles applied by the writer of the transpose.  Warps (0, 1)
-// take component 0, warps (2, 3) component 1.  Same-box A/B (cycles per step):
-// GC = 1 5.78k -> 5.37k, GC = 2 7.99k -> 7.61k, GC = 3 10.40k -> 10.07k against two
-// inverting warps per gate (profiles/r02_v5_ipair_ab.txt, r02_v5_ipair_gc23_ab.txt).
-// Rejected on the same box: four warps on quarter problems with a shuffle radix-2
-// (GC = 1 5.81k), pairs across the two gates of a CTA (GC = 2 8.23k), gate stagger
-// (+1.9-2.8 % with the two-warp inverse, +0.1-1 % with pairs: profiles/r02_v5_stagger_pairs_ab.txt),
-// loader nanosleep back-off (+0.7-1.7 % at GC = 2, 3).
-// Digit extraction with every accumulator load hoisted above the arithmetic and the
-// partner stores (bit GC-1).  Same-box A/B, cycles per step: GC = 1 5.35k -> 5.23k,
-// GC = 2 7.61k -> 7.66k (off there), GC = 3 10.07k -> 10.03k (profiles/r02_v5_digit_hoist_ab.txt)
-#ifndef GW_V5_DIGITS_HOIST
-#define GW_V5_DIGITS_HOIST 5
-#endif
-// MAC phase with the V stores of both frequency pairs after both MACs (bit GC-1).
-// Same-box A/B, cycles per step: GC = 1 5.22k -> 5.11k; GC = 2, 3 +0.2 % (off there)
-// (profiles/r02_v5_mac_defer_ab.txt)
-// B3 as a barrier of the inverting pair only (bit GC-1), with V_1 in U row 2 and each
-// pair's scratch in its own odd row.  Same-box A/B, cycles per step: GC = 1 5.12k -> 5.03k,
-// GC = 2 7.72k -> 7.59k, GC = 3 10.02k -> 9.93k (profiles/r02_v5_pair_b3_ab.txt)
-#ifndef GW_V5_PAIR_B3
-#define GW_V5_PAIR_B3 7
-#endif
-#ifndef GW_V5_M_DEFER
-#define GW_V5_M_DEFER 1
-#endif
+// ---- design switches (compile-time; every default is a same-box A/B, profiles/r02_v5_*) ----
+//
+// The inverse is always the paired split inverse: two warps of a gate invert one
+// accumulator component together, each doing the odd or even outputs of both DFT-16
+// passes (decimation in frequency), with the lane twiddles applied by the writer of the
+// transpose; warps (0, 1) take component 0, warps (2, 3) component 1.  Against two inverting
+// warps per gate: GC = 1 5.78k -> 5.37k, GC = 2 7.99k -> 7.61k, GC = 3 10.40k -> 10.07k
+// cycles per step (r02_v5_ipair_ab.txt, r02_v5_ipair_gc23_ab.txt).  Measured and not kept:
+// four warps on quarter problems with a shuffle radix-2 (GC = 1 5.81k), pairs across the
+// two gates of a CTA (GC = 2 8.23k), gate stagger (+0.1-2.8 %), loader nanosleep back-off
+// (+0.7-1.7 % at GC = 2, 3), the forward transpose through TMEM (+2-6 %,
+// r02_v5_tmem_transpose_rejected.txt), both pairs' MAC keys requested up front (+4.7 % at GC = 1).
+
 // MAC lanes own the frequency pair (c', c' + 8) (c' = 2w + lane / 16) instead of (c, c + 1),
-// so the MAC phase can hand the paired inverse its DIF-split inputs directly:
-// V[c'] + V[c' + 8] in slot c' and (V[c'] - V[c' + 8]) w16^(-c') in slot c' + 8, and each
-// inverting warp reads 8 values instead of 16.  Global (it changes the key image layout).
-// Same-box A/B, cycles per step: GC = 1 5.17k -> 4.97k, GC = 2 7.63k -> 7.40k,
-// GC = 3 10.01k -> 9.78k (profiles/r02_v5_msplit_ab.txt)
+// so the MAC phase hands the paired inverse its DIF-split inputs directly: V[c'] + V[c'+8]
+// in slot c' and (V[c'] - V[c'+8]) w16^(-c') in slot c'+8; each inverting warp reads 8
+// values instead of 16.  Global (it changes the key image layout).  GC = 1 5.17k -> 4.97k,
+// GC = 2 7.63k -> 7.40k, GC = 3 10.01k -> 9.78k (r02_v5_msplit_ab.txt)
 #ifndef GW_V5_MSPLIT
 #define GW_V5_MSPLIT 1
 #endif
+// End-of-step barrier of the inverting pair only (bit GC-1), with V_1 in U row 2 and each
+// pair's scratch in its own odd row.  GC = 1 5.12k -> 5.03k, GC = 2 7.72k -> 7.59k,
+// GC = 3 10.02k -> 9.93k (r02_v5_pair_b3_ab.txt)
+#ifndef GW_V5_PAIR_B3
+#define GW_V5_PAIR_B3 7
+#endif
+// Digit extraction with every accumulator load hoisted above the arithmetic and the
+// partner stores (bit GC-1).  GC = 1 5.35k -> 5.23k, GC = 2 7.61k -> 7.66k (off there),
+// GC = 3 10.07k -> 10.03k (r02_v5_digit_hoist_ab.txt)
+#ifndef GW_V5_DIGITS_HOIST
+#define GW_V5_DIGITS_HOIST 5
+#endif
+// MAC phase with the V stores of both frequency pairs after both MACs (bit GC-1; implied by
+// GW_V5_MSPLIT).  GC = 1 5.22k -> 5.11k; GC = 2, 3 +0.2 % (r02_v5_mac_defer_ab.txt)
+#ifndef GW_V5_M_DEFER
+#define GW_V5_M_DEFER 1
+#endif
 // L2 bulk prefetch of the key slab GW_V5_L2PF steps ahead (v3 uses 2).  With v5's 64 KB
-// slabs it does not pay: same-box A/B, distance 0 vs 2: -0.8 / -0.4 / -0.3 % per step at
-// GC = 1 / 2 / 3 with the key L2-resident, +0.2 % bench value with L2 flushed between steps
-// (profiles/r02_v5_l2pf_ab.txt)
+// slabs it does not pay: distance 0 vs 2: -0.8 / -0.4 / -0.3 % per step at GC = 1 / 2 / 3
+// with the key L2-resident, +0.2 % bench value with L2 flushed between steps (r02_v5_l2pf_ab.txt)
 #ifndef GW_V5_L2PF
 #define GW_V5_L2PF 0
 #endif
