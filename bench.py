@@ -263,6 +263,21 @@ class CpuReference:
                 lat.append(time.perf_counter() - t0)
             res[name] = {"app_latency_s": statistics.median(lat), "gates": len(c.gates), "repeats": repeats}
         res["total_app_latency_s"] = sum(v["app_latency_s"] for v in res.values())
+        # the same two circuits as one netlist through the reference's own parser and runtime
+        c = NL.merge_circuits([("add", C.gen_adder(8)), ("mul", NL.gen_multiplier(8))])
+        vals = {p.name: int(rng.integers(0, 1 << p.width)) for p in c.inputs}
+        srng = SeededRng(8100)
+        inputs = {p.name: encrypt_bits(PARAM_128, self.ks.lwe_sk, C.value_to_bits(vals[p.name], p.width),
+                                       srng) for p in c.inputs}
+        rcirc = self.rcirc.parse_circuit(C.serialize_circuit(c))
+        sched = self.rsch.build_schedule(rcirc, self.cores)
+        lat = []
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            self.rrt.evaluate(rcirc, sched, inputs, self.rks)
+            lat.append(time.perf_counter() - t0)
+        res["combined_netlist"] = {"app_latency_s": statistics.median(lat), "gates": len(c.gates),
+                                   "repeats": repeats}
         res["workers"] = self.cores
         return res
 
@@ -357,6 +372,33 @@ def config2_latency(ks, P, eng, repeats: int = 5):
                      "device_time_s": met.device_time_seconds, "wall_runs_s": lat,
                      "evaluate_wall_s": met.wall_time_seconds, "host_phases_s": phases, "decrypt_ok": ok}
     res["total_app_latency_s"] = sum(v["app_latency_s"] for v in res.values())
+    # the two circuits as ONE level-scheduled netlist (netlists.merge_circuits): their level-k
+    # gates share each level's launch, so the evaluation takes as many levels as the deeper one
+    c = NL.merge_circuits([("add", C.gen_adder(8)), ("mul", NL.gen_multiplier(8))])
+    rng = np.random.default_rng(81)
+    vals = {p.name: int(rng.integers(0, 1 << p.width)) for p in c.inputs}
+    srng = SeededRng(8100)
+    inputs = {p.name: encrypt_bits(P, ks.lwe_sk, C.value_to_bits(vals[p.name], p.width), srng)
+              for p in c.inputs}
+    sched = build_schedule(c, 1)
+    evaluate(c, sched, inputs, ks)  # warm
+    lat = []
+    for _ in range(repeats):
+        gc.collect()
+        gc.disable()
+        try:
+            t0 = time.perf_counter()
+            outs, met = evaluate(c, sched, inputs, ks)
+            lat.append(time.perf_counter() - t0)
+        finally:
+            gc.enable()
+    plain = C.simulate_plain(c, vals)
+    ok = all(C.bits_to_value(decrypt_rows(ks.lwe_sk, outs[k])) == v for k, v in plain.items())
+    res["combined_netlist"] = {"app_latency_s": statistics.median(lat), "gates": len(c.gates),
+                               "levels": len(sched.waves), "device_time_s": met.device_time_seconds,
+                               "wall_runs_s": lat, "decrypt_ok": ok,
+                               "note": "adder8 and multiplier8 side by side in one netlist "
+                                       "(netlists.merge_circuits), one level-scheduled evaluation"}
     return res
 
 

@@ -246,3 +246,30 @@ def hard_sigmoid_plain(c: int, w: int, frac: int) -> int:
 def to_signed(v: int, w: int) -> int:
     v &= (1 << w) - 1
     return v - (1 << w) if v >> (w - 1) else v
+
+
+def merge_circuits(parts) -> Circuit:
+    """Independent circuits side by side in ONE netlist: `parts` is a sequence of
+    (prefix, circuit); ports become "<prefix>_<name>", input wires are renumbered in
+    declaration order (the text format's rule) and every gate gets a fresh id after
+    all inputs.  A level scheduler then runs the circuits' level-k gates together
+    (config 2: the adder and the multiplier in one evaluation)."""
+    inputs, outputs, gates = [], [], []
+    nxt = 0
+    maps = []
+    for prefix, c in parts:
+        m = {}
+        for p in c.inputs:
+            new = tuple(range(nxt, nxt + p.width))
+            nxt += p.width
+            m.update(zip(p.wires, new))
+            inputs.append(Port(f"{prefix}_{p.name}", new))
+        maps.append(m)
+    for (prefix, c), m in zip(parts, maps):
+        for g in c.gates:
+            m[g.id] = nxt
+            nxt += 1
+            gates.append(Gate(m[g.id], g.opcode, tuple(m[w] for w in g.operands)))
+        for p in c.outputs:
+            outputs.append(Port(f"{prefix}_{p.name}", tuple(m[w] for w in p.wires)))
+    return Circuit(tuple(inputs), tuple(outputs), tuple(gates))

@@ -87,6 +87,16 @@ def test_config2_adder8_every_gate(p128_keys):
     assert checked == len(c.gates) == 40 and met.bootstrap_count == 39
 
 
+def test_config2_combined_netlist_every_gate(p128_keys):
+    """Config 2's two circuits as ONE level-scheduled netlist (netlists.merge_circuits):
+    35 levels, every gate recomputed by the oracle from the GPU's operands, bit-exact."""
+    from paper_2306_11006_b200 import circuit as C
+    from paper_2306_11006_b200 import netlists as NL
+    c = NL.merge_circuits([("add", C.gen_adder(8)), ("mul", NL.gen_multiplier(8))])
+    met, checked, _ = _run_and_sample(c, 82, p128_keys, samples=None)
+    assert checked == len(c.gates) == 360 and met.bootstrap_count == 359
+
+
 def test_config4_fc_layer_sampled_and_margin(p128_keys):
     """Config 4 (fc layer 256 -> 30, w[30][256]: 11.79M gates, 117 levels, the
     largest single-GPU workload): every decrypted output exact, 16 sampled

@@ -78,3 +78,22 @@ def test_generated_netlists_are_wide_and_shallow():
     assert len(c.gates) > 20000
     assert w.depth < 120
     assert max(len(x) for x in w.order) > 2000
+
+
+def test_merge_circuits_side_by_side():
+    """Two independent circuits in one netlist: same outputs as each alone, valid,
+    text round trip, levels = the deeper circuit's."""
+    from paper_2306_11006_b200.scheduler import build_schedule
+    a, m = C.gen_adder(8), NL.gen_multiplier(8)
+    mc = NL.merge_circuits([("add", a), ("mul", m)])
+    assert not C.validate(mc)
+    assert C.parse_circuit(C.serialize_circuit(mc)) == mc
+    assert len(mc.gates) == len(a.gates) + len(m.gates)
+    assert len(build_schedule(mc, 1).waves) == max(len(build_schedule(a, 1).waves), len(build_schedule(m, 1).waves))
+    rng = np.random.default_rng(5)
+    for _ in range(20):
+        vals = {p.name: int(rng.integers(0, 1 << p.width)) for p in mc.inputs}
+        out = C.simulate_plain(mc, vals)
+        oa = C.simulate_plain(a, {k[4:]: v for k, v in vals.items() if k.startswith("add_")})
+        om = C.simulate_plain(m, {k[4:]: v for k, v in vals.items() if k.startswith("mul_")})
+        assert out == {**{"add_" + k: v for k, v in oa.items()}, **{"mul_" + k: v for k, v in om.items()}}
