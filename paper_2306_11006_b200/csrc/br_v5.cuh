@@ -34,6 +34,7 @@
 // twiddles (2 x 32 columns).  The loader warps run up to two steps ahead of the
 // MAC: slab i waits for MAC(i - 3) to release its slot.
 #pragma once
+
 #include "br_v3.cuh"
 
 namespace gw {
@@ -104,6 +105,18 @@ __host__ __device__ __forceinline__ size_t v5_index(int i, int cidx, int tlane) 
 // with the key L2-resident, +0.2 % bench value with L2 flushed between steps (r02_v5_l2pf_ab.txt)
 #ifndef GW_V5_L2PF
 #define GW_V5_L2PF 0
+#endif
+// F-phase digit conversion specialised on the warp's half (GC >= GW_V5_HH_BRANCH; 0 = never):
+// one warp-uniform branch instead of 32 SELs.  GC = 1 +4 % (worse), GC = 2 -0.2 %, GC = 3 -0.6 %
+// cycles per step (r02_v5_conv_ab.txt)
+#ifndef GW_V5_HH_BRANCH
+#define GW_V5_HH_BRANCH 2
+#endif
+// digit -> double as an integer subtract + I2F.F64 instead of the magic-number DADD, for
+// GC >= GW_V5_CONV_I2F (0 = never).  Pays only together with the branch, at GC = 3: -0.3 %
+// there, +0.7 / +1.3 % at GC = 2 / 1 (r02_v5_conv_ab.txt)
+#ifndef GW_V5_CONV_I2F
+#define GW_V5_CONV_I2F 3
 #endif
 #ifndef GW_V5_RED
 #define GW_V5_RED 1  // accumulator updates as shared-memory RED.ADD (same-box A/B: -0.4 / -0.7 / -1 % at GC = 1 / 2 / 3 vs load-add-store, profiles/r02_v5_stagger_red_ab.txt)
@@ -338,17 +351,36 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
           }
         }
         named_barrier(5 + 2 * gl + cr, 64);
+        // digit (offset by half the base) -> double: the magic-number DADD, or (GW_V5_CONV_I2F)
+        // an integer subtract and an int -> double conversion
+        constexpr bool kI2F = GW_V5_CONV_I2F > 0 && GC >= GW_V5_CONV_I2F;
+        constexpr bool kHHBranch = GW_V5_HH_BRANCH > 0 && GC >= GW_V5_HH_BRANCH;
+        auto dconv = [&](uint32_t u) -> double {
+          if constexpr (kI2F) return __int2double_rn((int)u - half_base);
+          else return digit_to_double_lo(u, dmagic);
+        };
+        // (re, im) = (digit of j, digit of j + M): the level-warp of half hh computed its own
+        // level's digits for half hh and received the partner's for the other half
+        auto convert = [&](auto sel) {
+          const bool upper = sel();
 #pragma unroll
-        for (int m1 = 0; m1 < P; m1 += 2) {
-          const uint32_t w = from_partner[(m1 / 2) * 32 + lane];
+          for (int m1 = 0; m1 < P; m1 += 2) {
+            const uint32_t w = from_partner[(m1 / 2) * 32 + lane];
 #pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const uint32_t rv = q ? (w >> 16) : (w & 0xFFFFu);
-            const uint32_t re = hh ? rv : mine[m1 + q], im = hh ? mine[m1 + q] : rv;
-            double2 v = make_double2(digit_to_double_lo(re, dmagic), digit_to_double_lo(im, dmagic));
-            if (m1 + q > 0) v = cmul(v, c_root64[G::CSTEP * (m1 + q)]);
-            x[bitrev_c<G::LOGP>(m1 + q)] = v;
+            for (int q = 0; q < 2; ++q) {
+              const uint32_t rv = q ? (w >> 16) : (w & 0xFFFFu);
+              const uint32_t re = upper ? rv : mine[m1 + q], im = upper ? mine[m1 + q] : rv;
+              double2 v = make_double2(dconv(re), dconv(im));
+              if (m1 + q > 0) v = cmul(v, c_root64[G::CSTEP * (m1 + q)]);
+              x[bitrev_c<G::LOGP>(m1 + q)] = v;
+            }
           }
+        };
+        if constexpr (kHHBranch) {
+          if (hh) convert([] { return true; });
+          else convert([] { return false; });
+        } else {
+          convert([&] { return hh != 0; });
         }
         double2* tile = U + (size_t)o * P * L;
         fft_forward_head<LOGN, true>(x, tile, TwTmemHalves{tm_tw}, l);
