@@ -37,6 +37,10 @@ struct BrArgs {
   const uint32_t* rows = nullptr;
   int64_t row_stride = 0;
   uint32_t mu = 0;
+  // L2 warm-up of the next kernel's operand (v5): over the last kL2WarmSteps steps each CTA
+  // prefetches its 1/gridDim share of these bytes (the keyswitch key image) into L2
+  const char* l2warm = nullptr;
+  uint64_t l2warm_bytes = 0;
 };
 
 // Bootstrapping key, FFT domain: [i][c][h][s][r][lane] complex, scaled by 1/M.

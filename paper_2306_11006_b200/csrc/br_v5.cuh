@@ -118,6 +118,11 @@ __host__ __device__ __forceinline__ size_t v5_index(int i, int cidx, int tlane) 
 #ifndef GW_V5_CONV_I2F
 #define GW_V5_CONV_I2F 3
 #endif
+// steps at the end of the blind rotation over which the loader warps warm L2 with the
+// keyswitch key image (BrArgs::l2warm)
+#ifndef GW_V5_L2WARM_STEPS
+#define GW_V5_L2WARM_STEPS 32
+#endif
 #ifndef GW_V5_RED
 #define GW_V5_RED 1  // accumulator updates as shared-memory RED.ADD (same-box A/B: -0.4 / -0.7 / -1 % at GC = 1 / 2 / 3 vs load-add-store, profiles/r02_v5_stagger_red_ab.txt)
 #endif
@@ -138,6 +143,7 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
   using G = V5::G;
   constexpr int N = V5::N, M = V5::M, P = V5::P, L = V5::L, R = V5::R, LEV = V5::LEV, LOGN = V5::LOGN;
   constexpr int UB = V5::UB, COLS = V5::COLS, CIDX = V5::CIDX, NSLOT = V5::NSLOT;
+  constexpr int kL2WarmSteps = GW_V5_L2WARM_STEPS;
   constexpr int TWCOL = V5::TWCOL, TW4COL = V5::TW4COL;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -264,6 +270,17 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf), "r"(V5::SLAB) : "memory");
       }
 #endif
+      if (o == 3 && lane == 0 && a.l2warm_bytes && i >= a.n - kL2WarmSteps) {
+        // this CTA's share of the keyswitch key image, one chunk per remaining step
+        const uint64_t share = ((a.l2warm_bytes + gridDim.x - 1) / gridDim.x + 15) & ~15ull;
+        const uint64_t chunk = ((share + kL2WarmSteps - 1) / kL2WarmSteps + 15) & ~15ull;
+        const uint64_t lo = (uint64_t)blockIdx.x * share + (uint64_t)(i - (a.n - kL2WarmSteps)) * chunk;
+        const uint64_t hi = min(min(lo + chunk, (uint64_t)(blockIdx.x + 1) * share), a.l2warm_bytes);
+        for (uint64_t p = lo; p < hi; p += 65536) {
+          const uint32_t len = (uint32_t)min(hi - p, (uint64_t)65536);
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.l2warm + p), "r"(len) : "memory");
+        }
+      }
       if (i >= NSLOT) {
         mbar_wait(&empty_bar[slot], (uint32_t)(((i - NSLOT) / NSLOT) & 1));
         tm_fence_after();

@@ -60,6 +60,8 @@ struct gw_ctx {
   uint32_t* ksk = nullptr;
   uint8_t* kimg = nullptr;     // keyswitch key as INT8 tensor-core B image (ks_tc.cuh)
   int kt_ntiles = 0, kt_kblocks = 0;
+  size_t kimg_bytes = 0;
+  bool ks_l2warm = true;        // v5 warms L2 with the key image before the keyswitch (GATEWAVE_KS_L2WARM)
   bool ks_tc = false;          // tensor-core keyswitch usable for these parameters
   int ks_variant = 1;          // 1: tensor cores when usable, 0: CUDA cores (GATEWAVE_KS_KERNEL=cuda)
   uint32_t* ks_ut = nullptr;   // (N, count) rounded samples
@@ -607,6 +609,10 @@ int run_level(gw_ctx* c, const uint32_t* src, int64_t src_stride, uint32_t* dst,
     a.gates_per_cta = 1;
     a.prof = c->br_prof;
     a.ablate = c->br_ablate;
+    if (c->ks_l2warm && c->ks_tc && c->ks_variant && c->kimg) {
+      a.l2warm = reinterpret_cast<const char*>(c->kimg);
+      a.l2warm_bytes = c->kimg_bytes;
+    }
     if ((rc = staged(c, 0, J, [&] { return launch_br(c, a); }))) return rc;
     if ((rc = staged(c, 1, U, [&] { return launch_ks(c, c->acc, units, U, dst, dst_stride); }))) return rc;
   }
@@ -794,6 +800,7 @@ int gw_create(int device, gw_ctx** out) {
   if (const char* v = getenv("GATEWAVE_BR_LDR")) c->br_ldr = atoi(v) != 0;
   if (const char* v = getenv("GATEWAVE_BR_UNFUSED")) c->br_unfused = atoi(v) != 0;
   if (const char* v = getenv("GATEWAVE_BR_EXACT")) c->br_exact = atoi(v) != 0;
+  if (const char* v = getenv("GATEWAVE_KS_L2WARM")) c->ks_l2warm = atoi(v) != 0;
 
   if (const char* v = getenv("GATEWAVE_BR_KERNEL"))
     c->br_variant = strcmp(v, "v1") == 0 ? 0 : strcmp(v, "v2") == 0 ? 1 : 2;
@@ -1012,6 +1019,7 @@ int gw_upload_keys(gw_ctx* c, const uint32_t* bk_coeff, const uint32_t* ksk) {
       c->kt_kblocks = (int)((size_t)N * t / KT_PAIRS);
       const size_t bytes = (size_t)c->kt_ntiles * c->kt_kblocks * KT_B_BYTES;
       GW_CUDA(c, cudaMalloc(&c->kimg, bytes));
+      c->kimg_bytes = bytes;
       const size_t chunks = bytes / 16;
       k_ksk_to_tc<<<(unsigned)((chunks + 255) / 256), 256, 0, c->stream>>>(c->ksk, N, t, V, n + 1, c->Wp,
                                                                            c->kt_ntiles, c->kt_kblocks, c->kimg);

@@ -1,0 +1,9 @@
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+timeout 1200 python -m pytest tests/test_gpu_keyswitch.py tests/test_gpu_parity.py tests/test_gpu_large_batch.py -x -q 2>&1 | tail -3
+for rep in 1 2 3; do for m in 0 1; do
+  GATEWAVE_KS_MT2=$m timeout 600 python bench.py --no-cpu-baseline --no-netlist --no-cpu-netlists --steps 30 --warmup 5 2>/dev/null | tail -1 | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']
+print('mt2=$m value %.0f e2e %.0f ms/step %.4f br %.4f ks %.4f' % (d['value'], d['e2e']['value'], d['ms_per_step'], r['per_launch_ms'], r['keyswitch_ms_per_launch']))"
+done; done
+ncu --set full --import-source on --clock-control none -k regex:k_keyswitch_tc -s 1 -c 1 -o gpurun_out/ks3_cold python tools/ks_once.py > gpurun_out/ks3_ncu.log 2>&1
+tail -2 gpurun_out/ks3_ncu.log
