@@ -609,7 +609,9 @@ int run_level(gw_ctx* c, const uint32_t* src, int64_t src_stride, uint32_t* dst,
     a.gates_per_cta = 1;
     a.prof = c->br_prof;
     a.ablate = c->br_ablate;
-    if (c->ks_l2warm && c->ks_tc && c->ks_variant && c->kimg) {
+    // wide launches only: with a few CTAs each would prefetch megabytes, and the narrow
+    // levels of config 2 measured 10 % slower with it (profiles/r02_keyswitch_ab.txt)
+    if (c->ks_l2warm && c->ks_tc && c->ks_variant && c->kimg && J >= c->sm_count) {
       a.l2warm = reinterpret_cast<const char*>(c->kimg);
       a.l2warm_bytes = c->kimg_bytes;
     }

@@ -10,6 +10,7 @@ import ctypes
 import functools
 import os
 import threading
+import weakref
 from collections import OrderedDict
 
 import numpy as np
@@ -89,8 +90,8 @@ def load_library(path: str | None = None):
             "gw_download_bk_fft": ([_P, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
             "gw_blind_rotate": ([_P, _U32P, ctypes.c_int64, _U32P, _U32P], ctypes.c_int),
             "gw_keyswitch": ([_P, _U32P, ctypes.c_int64, _U32P], ctypes.c_int),
-            "gw_eval_gate_batch": ([_P, ctypes.c_int, ctypes.POINTER(_U32P), ctypes.c_int,
-                                    ctypes.c_int64, _U32P], ctypes.c_int),
+            "gw_eval_gate_batch": ([_P, ctypes.c_int, ctypes.POINTER(_P), ctypes.c_int,
+                                    ctypes.c_int64, _P], ctypes.c_int),
             "gw_eval_gate_batch_device": ([_P, ctypes.c_int, ctypes.POINTER(_P), ctypes.c_int64,
                                            ctypes.c_int, ctypes.c_int64, _P, ctypes.c_int64],
                                           ctypes.c_int),
@@ -148,6 +149,11 @@ def device_count() -> int:
 
 def _u32(a):
     return a.ctypes.data_as(_U32P)
+
+
+def _addr(a) -> int:
+    """Data address of a numpy array (cheaper than a ctypes pointer object)."""
+    return a.__array_interface__["data"][0]
 
 
 def _c_rows(a, width=None):
@@ -357,9 +363,9 @@ class Engine:
         out = _host_rows(count, self.n + 1)
         if count == 0:
             return out
-        arr = (_U32P * max(1, len(mats)))(*[_u32(m) for m in mats])
+        arr = (_P * max(1, len(mats)))(*[_addr(m) for m in mats])
         self._check(self._lib.gw_eval_gate_batch(self._ctx, opcode, arr, len(mats), count,
-                                                 _u32(out)))
+                                                 _addr(out)))
         return out
 
     def eval_gate_batch_device(self, opcode: int, d_ops, in_stride: int, count: int, d_out: int,
@@ -535,6 +541,13 @@ def set_device(device: int):
 def default_device() -> int:
     if _device_override is not None:
         return _device_override
+    env = getattr(os.environ, "_data", None)  # CPython's bytes mapping: no per-lookup encoding
+    if env is not None and os.name == "posix":
+        for var in (b"GATEWAVE_DEVICE", b"LOCAL_RANK"):
+            v = env.get(var)
+            if v is not None:
+                return int(v)
+        return 0
     for var in ("GATEWAVE_DEVICE", "LOCAL_RANK"):
         if var in os.environ:
             return int(os.environ[var])
@@ -612,9 +625,30 @@ def key_digest(a) -> str:
     return d
 
 
+_FAST: dict[tuple, tuple] = {}   # (ids of params/bk/ksk, device) -> (weakref to engine, params, bk, ksk)
+
+
 def engine_for(params, bk_data=None, ksk_data=None, device: int | None = None) -> Engine:
-    """Context with these keys resident, uploaded once and cached by content."""
+    """Context with these keys resident, uploaded once and cached by content.
+    Repeated calls with the same (read-only) key arrays skip the digest lookup."""
     dev = default_device() if device is None else int(device)
+    fk = (id(params), id(bk_data), id(ksk_data), dev)
+    hit = _FAST.get(fk)
+    if hit is not None:
+        ref, p, b, k = hit
+        eng = ref()
+        if eng is not None and p is params and b is bk_data and k is ksk_data and eng.handle.value and \
+                (b is None or _frozen(b)) and (k is None or _frozen(k)):
+            return eng
+    eng = _engine_for_slow(params, bk_data, ksk_data, dev)
+    with _cache_lock:
+        if len(_FAST) >= 16:
+            _FAST.clear()
+        _FAST[fk] = (weakref.ref(eng), params, bk_data, ksk_data)
+    return eng
+
+
+def _engine_for_slow(params, bk_data, ksk_data, dev: int) -> Engine:
     with _cache_lock:
         key = (params_tuple(params), dev,
                None if bk_data is None else key_digest(bk_data),
@@ -637,3 +671,4 @@ def clear_cache():
             eng.close()
         _CACHE.clear()
         _DIGESTS.clear()
+        _FAST.clear()

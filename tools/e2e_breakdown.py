@@ -38,16 +38,16 @@ def timed(fn, n=40):
     return statistics.median(ts) * 1e6
 
 
-arr = (E._U32P * 2)(E._u32(pa), E._u32(pb))
+arr = (E._P * 2)(E._addr(pa), E._addr(pb))
 res = {
     "cggi.eval_gate_batch": timed(lambda: eval_gate_batch(GateKind.NAND, [pa, pb], ek)),
     "Engine.eval_gate_batch": timed(lambda: eng.eval_gate_batch(nand, [pa, pb], 256)),
-    "C gw_eval_gate_batch (ctypes)": timed(lambda: eng._lib.gw_eval_gate_batch(eng._ctx, nand, arr, 2, 256, E._u32(out))),
+    "C gw_eval_gate_batch (ctypes)": timed(lambda: eng._lib.gw_eval_gate_batch(eng._ctx, nand, arr, 2, 256, E._addr(out))),
 }
 eng.set_profiling(True)
 eng.stage_times(reset=True)
 for _ in range(20):
-    eng._lib.gw_eval_gate_batch(eng._ctx, nand, arr, 2, 256, E._u32(out))
+    eng._lib.gw_eval_gate_batch(eng._ctx, nand, arr, 2, 256, E._addr(out))
 st = eng.stage_times(reset=True)
 eng.set_profiling(False)
 res["device kernels (sum of stages)"] = sum(v[0] for v in st.values()) / 20 * 1e3
