@@ -444,7 +444,7 @@ constexpr int KS_GT = 16;
 int launch_ks(gw_ctx* c, const uint32_t* acc, const KsUnit* units, int U, uint32_t* out, int64_t out_stride) {
   if (U <= 0) return GW_OK;
   const int N = c->p.N, W = c->p.n + 1;
-  {
+  if (!(c->ks_tc && c->ks_variant)) {  // the tensor-core path zeroes in k_ks_prep
     dim3 grid((W + 255) / 256, grid_rows(U));
     k_zero_units<<<grid, 256, 0, c->stream>>>(units, U, out, out_stride, W);
     GW_LAUNCHED(c);
@@ -458,7 +458,7 @@ int launch_ks(gw_ctx* c, const uint32_t* acc, const KsUnit* units, int U, uint32
     {
       dim3 grid((U + 127) / 128, N);
       k_ks_prep<<<grid, 128, 0, c->stream>>>(acc, units, U, N, c->p.ks_levels * c->p.ks_base_bits, c->ks_ut,
-                                             (int64_t)ut_stride, body);
+                                             (int64_t)ut_stride, body, out, out_stride, W);
       GW_LAUNCHED(c);
     }
     KtArgs k;

@@ -229,13 +229,16 @@ __global__ void __launch_bounds__(KT_THREADS, 1) k_keyswitch_tc(KtArgs a) {
 
 // Rounded samples u = (ext[i] + 2^(31 - t*gamma)) >> (32 - t*gamma), transposed
 // (N, ut_stride), and body terms, from the accumulators (fused extraction and
-// MUX combine, cggi.py:695-704, 842-845).
+// MUX combine, cggi.py:695-704, 842-845).  Also zeroes the output rows the
+// keyswitch's split-K atomics add into (one launch fewer per level).
 __global__ void k_ks_prep(const uint32_t* __restrict__ acc, const KsUnit* __restrict__ units, int count, int N,
-                          int tg, uint32_t* __restrict__ ut, int64_t ut_stride, uint32_t* __restrict__ body) {
+                          int tg, uint32_t* __restrict__ ut, int64_t ut_stride, uint32_t* __restrict__ body,
+                          uint32_t* __restrict__ out, int64_t out_stride, int W) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y;
   if (g >= count) return;
   const KsUnit un = units[g];
+  for (int col = i; col < W; col += N) out[(size_t)un.out_row * out_stride + col] = 0u;
   const uint32_t* a0 = acc + (size_t)un.job0 * 2 * N;
   uint32_t x = (i == 0) ? a0[0] : 0u - a0[N - i];
   if (un.job1 >= 0) {
