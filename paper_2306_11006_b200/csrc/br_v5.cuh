@@ -123,6 +123,12 @@ __host__ __device__ __forceinline__ size_t v5_index(int i, int cidx, int tlane) 
 #ifndef GW_V5_L2WARM_STEPS
 #define GW_V5_L2WARM_STEPS 32
 #endif
+// loader warps wait for a free key slot with a try_wait suspend-time hint (ns; 0 = plain
+// try_wait loop; compiles to NANOSLEEP.SYNCS, woken by the barrier): GC = 1 -0.6 % per step,
+// GC = 2, 3 neutral for hints 200-20000 ns (r02_v5_ldr_hint_ab.txt)
+#ifndef GW_V5_LDR_HINT_NS
+#define GW_V5_LDR_HINT_NS 200
+#endif
 #ifndef GW_V5_RED
 #define GW_V5_RED 1  // accumulator updates as shared-memory RED.ADD (same-box A/B: -0.4 / -0.7 / -1 % at GC = 1 / 2 / 3 vs load-add-store, profiles/r02_v5_stagger_red_ab.txt)
 #endif
@@ -282,7 +288,10 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
         }
       }
       if (i >= NSLOT) {
-        mbar_wait(&empty_bar[slot], (uint32_t)(((i - NSLOT) / NSLOT) & 1));
+        if constexpr (GW_V5_LDR_HINT_NS > 0)
+          mbar_wait_hint<GW_V5_LDR_HINT_NS>(&empty_bar[slot], (uint32_t)(((i - NSLOT) / NSLOT) & 1));
+        else
+          mbar_wait(&empty_bar[slot], (uint32_t)(((i - NSLOT) / NSLOT) & 1));
         tm_fence_after();
       }
       const uint32_t dst = tm_warp + (uint32_t)(slot * COLS);

@@ -30,6 +30,28 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
+// try_wait with a suspend-time hint (ns): the thread may be suspended until the
+// phase completes or the hint elapses, instead of re-issuing the probe.
+template <uint32_t HINT_NS>
+__device__ __forceinline__ bool mbar_try_wait_hint(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "n"(HINT_NS)
+      : "memory");
+  return ok != 0;
+}
+template <uint32_t HINT_NS>
+__device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity) {
+  uint32_t spins = 0;
+  while (!mbar_try_wait_hint<HINT_NS>(bar, parity)) {
+    if (++spins > (1u << 24)) __trap();
+  }
+}
+
 // Wait for the phase with the given parity to complete.  Bounded: a protocol
 // bug traps (kernel error, context torn down) instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
