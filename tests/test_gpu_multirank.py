@@ -141,3 +141,23 @@ def test_nccl_library_binds():
     ver, why = nccl_available()
     assert ver >= 22700, why
     assert len(nccl_unique_id()) == 128
+
+
+def test_nccl_communicator_on_this_gpu():
+    """gw_nccl_init builds a real NCCL communicator on the device through the
+    run-time-bound library (world 1: the most one GPU allows), and a world-1
+    exchange plan enqueues as a no-op on it."""
+    import numpy as np
+    from paper_2306_11006_b200 import engine
+    from paper_2306_11006_b200.cggi import PARAM_128
+    ver, why = engine.nccl_available()
+    assert ver >= 22700, why
+    eng = engine.Engine(*engine.params_tuple(PARAM_128))
+    eng.nccl_init(1, 0, engine.nccl_unique_id())
+    xp = engine.ExchangePlanHandle(eng, np.zeros((2, 1, 1), np.int64), np.zeros(0, np.int64), 1, 0)
+    try:
+        xp.enqueue(0)
+        xp.enqueue(1)
+    finally:
+        xp.close()
+    eng.close()
