@@ -129,6 +129,11 @@ __host__ __device__ __forceinline__ size_t v5_index(int i, int cidx, int tlane) 
 #ifndef GW_V5_LDR_HINT_NS
 #define GW_V5_LDR_HINT_NS 200
 #endif
+// per-phase cycle counters (GATEWAVE_BR_PROFILE, tools/phase_profile.py) compiled in at
+// every GC (default: GC = 2 only); the predicated-off clock reads still cost issue slots
+#ifndef GW_V5_PHASE_PROF
+#define GW_V5_PHASE_PROF 0
+#endif
 #ifndef GW_V5_RED
 #define GW_V5_RED 1  // accumulator updates as shared-memory RED.ADD (same-box A/B: -0.4 / -0.7 / -1 % at GC = 1 / 2 / 3 vs load-add-store, profiles/r02_v5_stagger_red_ab.txt)
 #endif
@@ -252,7 +257,11 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
   const int pos = v3_pos(l);
   const int bar_id = 1 + gl;
 
-  const bool prof = a.prof != nullptr && blockIdx.x == 0 && gl == 0 && lane == 0;
+  // the (predicated-off) clock reads stay in at GC = 2, where they happen to steer the
+  // scheduler well: without them GC = 1 / 3 run 3.9 / 1.7 % faster, GC = 2 2 % slower
+  // (r02_v5_phase_marks_ab.txt)
+  constexpr bool kMarks = GW_V5_PHASE_PROF || GC == 2;
+  const bool prof = kMarks && a.prof != nullptr && blockIdx.x == 0 && gl == 0 && lane == 0;
   long long pt_[6] = {0, 0, 0, 0, 0, 0};
   long long tprev = clock64();
   auto mark = [&](int ph) {

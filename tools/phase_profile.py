@@ -1,4 +1,5 @@
-"""Per-phase cycle breakdown of the TMEM blind rotation (debug build flag)."""
+"""Per-phase cycle breakdown of the TMEM blind rotation (GATEWAVE_BR_PROFILE=1; for v5 at
+1 or 3 gates per SM build with -DGW_V5_PHASE_PROF=1, e.g. tools/build_variant.py)."""
 import os
 import sys
 
