@@ -134,6 +134,15 @@ __host__ __device__ __forceinline__ size_t v5_index(int i, int cidx, int tlane) 
 #ifndef GW_V5_PHASE_PROF
 #define GW_V5_PHASE_PROF 0
 #endif
+#ifndef GW_V5_MARK_MASK1
+#define GW_V5_MARK_MASK1 0
+#endif
+#ifndef GW_V5_MARK_MASK2
+#define GW_V5_MARK_MASK2 0x01
+#endif
+#ifndef GW_V5_MARK_MASK3
+#define GW_V5_MARK_MASK3 0
+#endif
 #ifndef GW_V5_RED
 #define GW_V5_RED 1  // accumulator updates as shared-memory RED.ADD (same-box A/B: -0.4 / -0.7 / -1 % at GC = 1 / 2 / 3 vs load-add-store, profiles/r02_v5_stagger_red_ab.txt)
 #endif
@@ -257,14 +266,18 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
   const int pos = v3_pos(l);
   const int bar_id = 1 + gl;
 
-  // the (predicated-off) clock reads stay in at GC = 2, where they happen to steer the
-  // scheduler well: without them GC = 1 / 3 run 3.9 / 1.7 % faster, GC = 2 2 % slower
-  // (r02_v5_phase_marks_ab.txt)
-  constexpr bool kMarks = GW_V5_PHASE_PROF || GC == 2;
+  // the (predicated-off) clock reads of the phase profiler cost issue slots and steer
+  // ptxas's schedule: without them GC = 1 / 3 run 3.9 / 1.7 % faster; at GC = 2 the first
+  // one alone (after the forward phase) gives the best schedule, 1.9 % faster than all six
+  // and 3.8 % faster than none (r02_v5_phase_marks_ab.txt).  -DGW_V5_PHASE_PROF=1 puts all
+  // six back at every GC for tools/phase_profile.py.
+  constexpr int kMarkMask = GW_V5_PHASE_PROF ? 0x3F : GC == 1 ? GW_V5_MARK_MASK1 : GC == 2 ? GW_V5_MARK_MASK2 : GW_V5_MARK_MASK3;
+  constexpr bool kMarks = kMarkMask != 0;
   const bool prof = kMarks && a.prof != nullptr && blockIdx.x == 0 && gl == 0 && lane == 0;
   long long pt_[6] = {0, 0, 0, 0, 0, 0};
   long long tprev = clock64();
   auto mark = [&](int ph) {
+    if (!((kMarkMask >> ph) & 1)) return;
     if (prof) {
       const long long t = clock64();
       pt_[ph] += t - tprev;
