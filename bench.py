@@ -514,7 +514,7 @@ def run_ours(args):
         gc = min(step_kcyc, key=lambda g: (-(-G // (sms * g)) * step_kcyc[g], g))
         kname = f"k_blind_rotate_v3<{gc}, {0 if gc == 4 else 2}, false>"
     else:
-        step_kcyc = {1: 4.75, 2: 7.22, 3: 9.52}          # gw_api.cu launch_v5 policy
+        step_kcyc = {1: 4.75, 2: 7.22, 3: 9.45}          # gw_api.cu launch_v5 policy
         gc = min(step_kcyc, key=lambda g: (-(-G // (sms * g)) * step_kcyc[g], g))
         kname = f"k_blind_rotate_v5<{gc}, false>"
     traffic = None

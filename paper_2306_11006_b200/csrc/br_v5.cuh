@@ -141,7 +141,7 @@ __host__ __device__ __forceinline__ size_t v5_index(int i, int cidx, int tlane) 
 #define GW_V5_MARK_MASK2 0x01
 #endif
 #ifndef GW_V5_MARK_MASK3
-#define GW_V5_MARK_MASK3 0
+#define GW_V5_MARK_MASK3 0x10
 #endif
 #ifndef GW_V5_RED
 #define GW_V5_RED 1  // accumulator updates as shared-memory RED.ADD (same-box A/B: -0.4 / -0.7 / -1 % at GC = 1 / 2 / 3 vs load-add-store, profiles/r02_v5_stagger_red_ab.txt)
@@ -269,7 +269,8 @@ __global__ void __launch_bounds__(128 * GC + 128, 1) k_blind_rotate_v5(BrArgs a)
   // the (predicated-off) clock reads of the phase profiler cost issue slots and steer
   // ptxas's schedule: without them GC = 1 / 3 run 3.9 / 1.7 % faster; at GC = 2 the first
   // one alone (after the forward phase) gives the best schedule, 1.9 % faster than all six
-  // and 3.8 % faster than none (r02_v5_phase_marks_ab.txt).  -DGW_V5_PHASE_PROF=1 puts all
+  // and 3.8 % faster than none; at GC = 3 the fifth alone (after the inverse), 0.75 % faster
+  // than none (r02_v5_phase_marks_ab.txt).  -DGW_V5_PHASE_PROF=1 puts all
   // six back at every GC for tools/phase_profile.py.
   constexpr int kMarkMask = GW_V5_PHASE_PROF ? 0x3F : GC == 1 ? GW_V5_MARK_MASK1 : GC == 2 ? GW_V5_MARK_MASK2 : GW_V5_MARK_MASK3;
   constexpr bool kMarks = kMarkMask != 0;

@@ -362,7 +362,7 @@ int launch_v5_g(gw_ctx* c, const BrArgs& a0) {
 // v5 (single key image): GC minimises waves x step time over the measured
 // per-step cycles of each configuration.
 int launch_v5(gw_ctx* c, const BrArgs& a) {
-  static const double kStep[4] = {0, 4.75, 7.22, 9.52};  // k cycles per step, profiles/r02_v5_phase_marks_ab.txt
+  static const double kStep[4] = {0, 4.75, 7.22, 9.45};  // k cycles per step, profiles/r02_v5_phase_marks_ab.txt
   int gc = 1;
   double best = 1e300;
   for (int g = 1; g <= 3; ++g) {
