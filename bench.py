@@ -69,7 +69,7 @@ def _args():
     ap.add_argument("--gates", type=int, default=GATES)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-netlist", action="store_true")
-    ap.add_argument("--sharded-timeout", type=float, default=1200.0,
+    ap.add_argument("--sharded-timeout", type=float, default=600.0,
                     help="deadline (s) for the sharded netlists at N > 1; on expiry the line is printed without them")
     ap.add_argument("--sharded", default="auto",
                     help="netlists evaluated sharded over the GPUs: auto (config4 at N>1, + config5 at "

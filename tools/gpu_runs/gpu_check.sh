@@ -1,6 +1,6 @@
 #!/bin/bash
 # One gpurun call: build check, GPU tests, bench (both arms), ncu launch list + full capture.
-# usage: tools/gpu_check.sh TAG [tests|bench|ncu ...]
+# usage: tools/gpu_runs/gpu_check.sh TAG [tests|bench|ncu ...]
 set -x
 TAG=${1:-run}; shift
 mkdir -p gpurun_out
