@@ -648,7 +648,7 @@ def run_ours(args):
         ref = CpuReference(G)
         ref.step()                                  # numba JIT warm (cached in NUMBA_CACHE_DIR)
         times, ref_out = [], None
-        for _ in range(2):
+        for _ in range(3):
             ref_out, dt = ref.step()
             times.append(dt)
         dt = statistics.median(times)
