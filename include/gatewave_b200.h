@@ -119,7 +119,9 @@ int gw_wires_put(gw_ctx* ctx, const int64_t* ids, const uint32_t* rows, int64_t 
 int gw_wires_get(gw_ctx* ctx, const int64_t* ids, uint32_t* rows, int64_t count);
 int gw_wires_device_ptr(gw_ctx* ctx, void** ptr, int64_t* stride_words);
 /* Use caller-owned device memory (e.g. a torch tensor) as the wire store:
- * `slots` rows of `stride_words` (= n+1 rounded up to 4) 32-bit words. */
+ * `slots` rows of `stride_words` (= n+1 rounded up to 4) 32-bit words.  The
+ * pointer must be device (or managed) memory on the context's GPU; host or
+ * other-GPU memory is rejected with GW_ERR_ARG (cudaPointerGetAttributes). */
 int gw_wires_attach(gw_ctx* ctx, void* dev_ptr, int64_t slots, int64_t stride_words);
 int gw_plan_create(gw_ctx* ctx, int64_t n_levels, const int64_t* level_offsets,
                    const int32_t* opcodes, const int32_t* operands /* (count, 3) */,

@@ -1278,6 +1278,15 @@ int gw_wires_attach(gw_ctx* c, void* dev_ptr, int64_t slots, int64_t stride_word
   if (!c->have_params) return fail(c, GW_ERR_STATE, "parameters not set");
   if (stride_words != c->Wp) return fail(c, GW_ERR_DIM, "wire rows must use the engine stride (n+1 rounded up to 4)");
   cudaSetDevice(c->device);
+  if (slots > 0) {  // the kernels dereference it on this context's device: reject anything else
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, dev_ptr) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, GW_ERR_ARG, "wire store pointer is not CUDA memory");
+    }
+    if ((a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) || a.device != c->device)
+      return fail(c, GW_ERR_ARG, "wire store must be device memory on GPU " + std::to_string(c->device));
+  }
   GW_CUDA(c, cudaStreamSynchronize(c->stream));
   if (c->wires_owned) cudaFree(c->wires);
   c->wires = (uint32_t*)dev_ptr;

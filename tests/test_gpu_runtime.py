@@ -184,3 +184,27 @@ def test_eval_key_file_feeds_the_device(p128_keys, tmp_path):
     b = encrypt_bits(PARAM_128, p128_keys.lwe_sk, rng.integers(0, 2, 40).astype(np.uint8), SeededRng(2))
     assert np.array_equal(eval_gate_batch(GateKind.XOR, [a, b], ek),
                           eval_gate_batch(GateKind.XOR, [a, b], p128_keys.eval_key()))
+
+
+def test_wires_attach_rejects_non_device_memory():
+    """gw_wires_attach takes only device memory on the context's own GPU: a host
+    (pinned) pointer is rejected before any kernel could dereference it; a
+    device tensor is accepted and evaluated into (foreign pointers)."""
+    import torch
+    from paper_2306_11006_b200.cggi import PARAM_128
+    from paper_2306_11006_b200.engine import Engine, params_tuple
+    eng = Engine(*params_tuple(PARAM_128), device=0)
+    stride = eng.row_stride
+    host = torch.zeros((8, stride), dtype=torch.int32, pin_memory=True)
+    with pytest.raises(ValueError, match="device memory"):
+        eng.wires_attach(host.data_ptr(), 8, stride)
+    plain = np.zeros((8, stride), np.int32)
+    with pytest.raises(ValueError):
+        eng.wires_attach(plain.ctypes.data, 8, stride)
+    dev = torch.zeros((8, stride), dtype=torch.int32, device="cuda:0")
+    eng.wires_attach(dev.data_ptr(), 8, stride)
+    rows = np.random.default_rng(2).integers(0, 2 ** 32, (3, PARAM_128.n + 1), dtype=np.uint32)
+    eng.wires_put(np.array([1, 4, 6]), rows)
+    assert np.array_equal(eng.wires_get(np.array([1, 4, 6])), rows)
+    eng.wires_attach(None, 0, stride)
+    eng.close()
