@@ -720,10 +720,14 @@ def run_ours(args):
         timer.cancel()
         if rank == 0:
             line["netlists_sharded"] = sharded
+    if dist is not None:
+        # Under NCCL_DEBUG=INFO NCCL logs each communicator's teardown to stdout: tear the
+        # engines' and torch's communicators down first so the JSON line is the last line.
+        from paper_2306_11006_b200 import engine as E
+        E.clear_cache()
+        dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.destroy_process_group()
     return 0
 
 
