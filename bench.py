@@ -725,7 +725,10 @@ def run_ours(args):
         # engines' and torch's communicators down first so the JSON line is the last line.
         from paper_2306_11006_b200 import engine as E
         E.clear_cache()
+        dist.barrier()                  # every rank's engine communicator is gone
         dist.destroy_process_group()
+        if rank == 0:
+            time.sleep(1.0)             # the other ranks' process-group teardown logs land first
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
